@@ -1,0 +1,123 @@
+/*
+ * bfgpu.h — C-ABI of the B200 backend for Blockbuster's fused block programs.
+ *
+ * The reference (arXiv 2505.07829, `blockfuse`) runs every fused candidate
+ * through one C++ entry point:
+ *
+ *   std::map<std::string, Matrix> blockfuse::execute(const BlockGraph& program,
+ *       const std::map<std::string, Matrix>& inputs, const DimBinding& binding,
+ *       const ExecOptions& opts = {});                 // proj/include/blockfuse/interpreter.hpp:478-487
+ *
+ * That walk (eval_graph -> eval_map -> eval_func, interpreter.hpp:263-472) is
+ * what this library replaces for the three fully fused programs that
+ * `fuse(lower(examples::X()))` emits (lowering.hpp:559-597, engine.hpp:164).
+ * The C++ adapter `bfgpu::execute` (host/bfgpu_execute.hpp) keeps the
+ * reference signature, recognizes the program and calls the entry points
+ * below. Everything here is plain C: device pointers, sizes, a stream.
+ *
+ * Conventions (all entry points):
+ *   - Matrices are dense row-major with the leading dimension equal to the
+ *     column count. "Transposed" right operands follow the reference's block
+ *     convention (lowering.hpp:159-169): Wt/Vt/Ut/Yt/K are [out, in], Vt for
+ *     attention is [Dv, Skv].
+ *   - All pointers are device pointers owned by the caller; outputs are
+ *     fully overwritten. `stream` is a cudaStream_t (NULL = legacy stream).
+ *   - Return BF_OK (0) on success, otherwise a BF_ERR_* code; the message is
+ *     available from bf_last_error() on the calling thread. This mirrors the
+ *     reference's `blockfuse::Error` exceptions (ir.hpp:20-23).
+ *   - Calls are reentrant per (device, stream); there is no global state
+ *     besides the per-thread error string and a launch counter.
+ *   - There is no CPU fallback: on a machine without an sm_100 GPU every
+ *     compute entry point fails with BF_ERR_UNSUPPORTED or BF_ERR_CUDA.
+ */
+#ifndef BFGPU_H_
+#define BFGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BF_API __attribute__((visibility("default")))
+#else
+#define BF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BF_OK 0
+#define BF_ERR_INVALID_ARGUMENT 1
+#define BF_ERR_UNSUPPORTED 2
+#define BF_ERR_CUDA 3
+#define BF_ERR_INTERNAL 4
+
+/* Element type of inputs and outputs. BF16 computes with fp32 accumulation
+ * on the tcgen05 tensor cores; F32 is the exact fp32-in/fp32-out mode (SIMT
+ * FMA, no TF32) that must match the float64 reference within 1e-4. */
+#define BF_DTYPE_BF16 0
+#define BF_DTYPE_F32 1
+
+/* K1 schedules. FUSED runs the whole program in one persistent kernel: the
+ * SwiGLU intermediate H travels through an L2-resident ring and is never
+ * written back to HBM in steady state (final snapshot, interpreter.hpp walk
+ * of fuse(lower(rms_ffn_swiglu()))). TWO_PHASE is the reference's first
+ * fusion snapshot (one internal buffered edge: H materialized in HBM). */
+#define BF_FFN_FUSED 0
+#define BF_FFN_TWO_PHASE 1
+
+/* ------------------------------------------------------------------------
+ * K1  Flash-RMSNorm + FFN-SwiGLU
+ *   O = (swish(r (.) X Wt^T) (.) (r (.) X Vt^T)) Ut^T,  r_i = 1/sqrt(mean_d X_i^2 + eps)
+ * Replaces: execute() on the final snapshot of fuse(lower(examples::rms_ffn_swiglu()))
+ *           (lowering.hpp:583-597; dense oracle ref::rms_ffn_swiglu, interpreter.hpp:553-559).
+ * Shapes: X[M,D], Wt[F,D], Vt[F,D], Ut[N,F], O[M,N]. D, F, N multiples of 8.
+ * eps = 0 reproduces the reference lowering (lowering.hpp:409-411).
+ * workspace: bf_rms_ffn_swiglu_workspace_bytes(...) bytes of device memory.
+ * ---------------------------------------------------------------------- */
+BF_API size_t bf_rms_ffn_swiglu_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule);
+BF_API int bf_rms_ffn_swiglu(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
+                      int64_t F, int64_t N, int dtype, float eps, int schedule, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K2  Flash-LayerNorm + MatMul
+ *   O = (X Yt^T - mu (x) colsum(Yt)) (.) rstd,  mu_i = mean_k X_ik,
+ *   rstd_i = 1/sqrt(mean_k X_ik^2 - mu_i^2 + eps)
+ * Replaces: execute() on the final snapshot of fuse(lower(examples::layernorm_matmul()))
+ *           (lowering.hpp:573-581; oracle ref::layernorm_matmul, interpreter.hpp:549-551).
+ * Shapes: X[M,K], Yt[N,K], O[M,N]. K, N multiples of 8. eps = 0 is the reference
+ * (no eps, no gamma/beta, lowering.hpp:350-363; sigma = 0 rows give NaN like
+ * the fused interpreter walk).
+ * ---------------------------------------------------------------------- */
+BF_API size_t bf_layernorm_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype);
+BF_API int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, int dtype, float eps,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K3  Rediscovered FlashAttention (non-causal, no mask), online softmax
+ *   O = softmax(scale * Q K^T) V, with V supplied as Vt[Dv, Skv]
+ * Replaces: execute() on the final snapshot of fuse(lower(examples::attention()))
+ *           (lowering.hpp:559-571) with the row-wise significand/exponent
+ *           rebasing of safe_attention_rows (safe_numerics.hpp:147-175).
+ * Shapes per head h in [0, BH): Q[Sq,D], K[Skv,D], Vt[Dv,Skv], O[Sq,Dv], heads
+ * stored back to back. scale <= 0 selects 1/sqrt(D) (the reference's scale).
+ * ---------------------------------------------------------------------- */
+BF_API int bf_attention(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
+                 int64_t D, int64_t Dv, int dtype, float scale, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Introspection
+ * ---------------------------------------------------------------------- */
+BF_API const char* bf_last_error(void);
+BF_API int bf_version(void);
+/* Total kernels this library launched in the process (for launch accounting). */
+BF_API uint64_t bf_kernel_launches(void);
+/* 1 if device `device` is an sm_100 part this build can run on. */
+BF_API int bf_device_supported(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BFGPU_H_ */

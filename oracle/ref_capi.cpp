@@ -1,0 +1,268 @@
+// TEST INFRASTRUCTURE — C wrapper over the UNMODIFIED reference headers.
+//
+// Built by oracle/Makefile from /root/reference/proj/include (read in place,
+// never copied) against the repo's Eigen-API stand-in
+// (third_party/eigen_shim), into oracle/_ref/libbfref.so. It exposes, as
+// plain C for ctypes:
+//   - the reference executor `blockfuse::execute` (interpreter.hpp:478) on any
+//     fusion snapshot of fuse(lower(examples::X())) (engine.hpp:164,
+//     lowering.hpp:559-597) or on the unfused lower() program;
+//   - the dense oracles ref::attention / layernorm_matmul / rms_ffn_swiglu
+//     (interpreter.hpp:543-559) and safe_attention_rows (safe_numerics.hpp:147);
+//   - random_inputs (interpreter.hpp:585), traffic_bytes and the structural
+//     metrics (metrics.hpp:15-50, 154-191), to_pseudocode (pseudocode.hpp:281).
+// Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg use it.
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "blockfuse/engine.hpp"
+#include "blockfuse/interpreter.hpp"
+#include "blockfuse/lowering.hpp"
+#include "blockfuse/metrics.hpp"
+#include "blockfuse/pseudocode.hpp"
+#include "blockfuse/safe_numerics.hpp"
+
+using namespace blockfuse;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_text;
+
+struct Programs {
+  BlockGraph unfused;
+  std::vector<BlockGraph> snapshots;
+};
+
+ArrayProgram example(int which) {
+  switch (which) {
+    case 0: return examples::attention();
+    case 1: return examples::layernorm_matmul();
+    case 2: return examples::rms_ffn_swiglu();
+  }
+  throw Error("unknown example " + std::to_string(which));
+}
+
+const Programs& programs(int which) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Programs>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(which);
+  if (it != cache.end()) return *it->second;
+  auto p = std::make_unique<Programs>();
+  p->unfused = lower(example(which));
+  FuseResult r = fuse(p->unfused);
+  for (auto& s : r.snapshots) p->snapshots.push_back(s.program);
+  return *cache.emplace(which, std::move(p)).first->second;
+}
+
+// snap >= 0: that snapshot; -1: final snapshot; -2: unfused lower() program.
+const BlockGraph& program(int which, int snap) {
+  const Programs& p = programs(which);
+  if (snap == -2) return p.unfused;
+  if (snap == -1) return p.snapshots.back();
+  if (snap < 0 || snap >= static_cast<int>(p.snapshots.size())) throw Error("snapshot index out of range");
+  return p.snapshots[static_cast<size_t>(snap)];
+}
+
+// "M=2x4,N=1x8" -> {M: count 2, len 4}, {N: count 1, len 8}
+DimBinding parse_binding(const char* spec) {
+  DimBinding b;
+  std::stringstream ss(spec ? spec : "");
+  std::string item;
+  while (std::getline(ss, item, ',')) {
+    if (item.empty()) continue;
+    auto eq = item.find('=');
+    auto x = item.find('x', eq);
+    if (eq == std::string::npos || x == std::string::npos) throw Error("bad binding item '" + item + "'");
+    b.dims[item.substr(0, eq)] = {std::stoi(item.substr(eq + 1, x - eq - 1)), std::stoi(item.substr(x + 1))};
+  }
+  return b;
+}
+
+Matrix from_rowmajor(const double* p, long rows, long cols) {
+  Matrix m(rows, cols);
+  for (long i = 0; i < rows; ++i)
+    for (long j = 0; j < cols; ++j) m(i, j) = p[i * cols + j];
+  return m;
+}
+
+void to_rowmajor(const Matrix& m, double* p) {
+  for (long i = 0; i < m.rows(); ++i)
+    for (long j = 0; j < m.cols(); ++j) p[i * m.cols() + j] = m(i, j);
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+__attribute__((visibility("default"))) const char* bfref_last_error() { return g_err.c_str(); }
+
+__attribute__((visibility("default"))) int bfref_num_snapshots(int which) {
+  int n = -1;
+  guarded([&] { n = static_cast<int>(programs(which).snapshots.size()); });
+  return n;
+}
+
+// internal buffered edges, top-level kernels, total node count of a program.
+__attribute__((visibility("default"))) int bfref_program_stats(int which, int snap, int* internal_buffered,
+                                                               int* kernels, int* nodes) {
+  return guarded([&] {
+    const BlockGraph& g = program(which, snap);
+    *internal_buffered = internal_buffered_edges(g);
+    *kernels = kernel_count(g);
+    *nodes = total_node_count(g);
+  });
+}
+
+__attribute__((visibility("default"))) unsigned long long bfref_traffic_bytes(int which, int snap, const char* binding,
+                                                                              int elem_bytes) {
+  unsigned long long v = 0;
+  if (guarded([&] {
+        TrafficModel tm;
+        tm.element_bytes = elem_bytes;
+        v = traffic_bytes(program(which, snap), parse_binding(binding), tm);
+      }))
+    return ~0ull;
+  return v;
+}
+
+__attribute__((visibility("default"))) const char* bfref_pseudocode(int which, int snap) {
+  g_text.clear();
+  guarded([&] { g_text = to_pseudocode(program(which, snap)); });
+  return g_text.c_str();
+}
+
+// Input names of the program in the order random_inputs draws them (sorted),
+// comma separated, with sizes "name:rows:cols".
+__attribute__((visibility("default"))) const char* bfref_input_specs(int which, const char* binding) {
+  g_text.clear();
+  guarded([&] {
+    auto specs = input_specs(program(which, -2), parse_binding(binding));
+    std::string s;
+    for (auto& sp : specs) {
+      if (!s.empty()) s += ",";
+      s += sp.name + ":" + std::to_string(sp.rows) + ":" + std::to_string(sp.cols);
+    }
+    g_text = s;
+  });
+  return g_text.c_str();
+}
+
+// random_inputs(input_specs(...), seed) written row-major into outs[i] in spec order.
+__attribute__((visibility("default"))) int bfref_random_inputs(int which, const char* binding,
+                                                               unsigned long long seed, double** outs) {
+  return guarded([&] {
+    auto specs = input_specs(program(which, -2), parse_binding(binding));
+    auto in = random_inputs(specs, seed);
+    for (size_t i = 0; i < specs.size(); ++i) to_rowmajor(in.at(specs[i].name), outs[i]);
+  });
+}
+
+// execute(program(which, snap), inputs, binding) -> output "O" row-major.
+__attribute__((visibility("default"))) int bfref_execute(int which, int snap, const char* binding, int n_inputs,
+                                                         const char** names, const double** data, const long* rows,
+                                                         const long* cols, double* out, long out_rows,
+                                                         long out_cols) {
+  return guarded([&] {
+    std::map<std::string, Matrix> in;
+    for (int i = 0; i < n_inputs; ++i) in[names[i]] = from_rowmajor(data[i], rows[i], cols[i]);
+    auto res = execute(program(which, snap), in, parse_binding(binding));
+    const Matrix& o = res.at("O");
+    if (o.rows() != out_rows || o.cols() != out_cols) throw Error("output shape mismatch");
+    to_rowmajor(o, out);
+  });
+}
+
+// Row-sharded execute: the first input (the row operand X or Q) and the output
+// are split into `shards` contiguous row blocks of rows[0]/shards rows; each
+// shard runs the reference executor with `shard_binding` on its own thread
+// (execute() is pure), at most `threads` at a time.
+__attribute__((visibility("default"))) int bfref_execute_rows(int which, int snap, const char* shard_binding,
+                                                              int n_inputs, const char** names, const double** data,
+                                                              const long* rows, const long* cols, double* out,
+                                                              long out_cols, int shards, int threads) {
+  return guarded([&] {
+    const BlockGraph& g = program(which, snap);
+    DimBinding b = parse_binding(shard_binding);
+    if (shards <= 0 || rows[0] % shards) throw Error("rows not divisible by shards");
+    const long srows = rows[0] / shards;
+    std::map<std::string, Matrix> shared;
+    for (int i = 1; i < n_inputs; ++i) shared[names[i]] = from_rowmajor(data[i], rows[i], cols[i]);
+    std::vector<std::string> errs(static_cast<size_t>(shards));
+    int next = 0;
+    std::mutex mu;
+    auto worker = [&] {
+      while (true) {
+        int s;
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (next >= shards) return;
+          s = next++;
+        }
+        try {
+          std::map<std::string, Matrix> in = shared;
+          in[names[0]] = from_rowmajor(data[0] + static_cast<long>(s) * srows * cols[0], srows, cols[0]);
+          auto res = execute(g, in, b);
+          to_rowmajor(res.at("O"), out + static_cast<long>(s) * srows * out_cols);
+        } catch (const std::exception& e) {
+          errs[static_cast<size_t>(s)] = e.what();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw Error(e);
+  });
+}
+
+// Dense oracles: which 0 ref::attention(Q,K,Vt), 1 ref::layernorm_matmul(X,Yt),
+// 2 ref::rms_ffn_swiglu(X,Wt,Vt,Ut,eps). Inputs in that order, row-major.
+__attribute__((visibility("default"))) int bfref_dense(int which, int n_inputs, const double** data, const long* rows,
+                                                       const long* cols, double eps, double* out) {
+  return guarded([&] {
+    std::vector<Matrix> m;
+    for (int i = 0; i < n_inputs; ++i) m.push_back(from_rowmajor(data[i], rows[i], cols[i]));
+    Matrix o;
+    if (which == 0)
+      o = ref::attention(m.at(0), m.at(1), m.at(2));
+    else if (which == 1)
+      o = ref::layernorm_matmul(m.at(0), m.at(1));
+    else if (which == 2)
+      o = ref::rms_ffn_swiglu(m.at(0), m.at(1), m.at(2), m.at(3), eps);
+    else
+      throw Error("unknown dense oracle");
+    to_rowmajor(o, out);
+  });
+}
+
+__attribute__((visibility("default"))) int bfref_safe_attention(const double* q, const double* k, const double* vt,
+                                                                long sq, long skv, long d, long dv, int row_chunks,
+                                                                double* out) {
+  return guarded([&] {
+    Matrix o = safe_attention_rows(from_rowmajor(q, sq, d), from_rowmajor(k, skv, d), from_rowmajor(vt, dv, skv),
+                                   row_chunks);
+    to_rowmajor(o, out);
+  });
+}
+
+}  // extern "C"

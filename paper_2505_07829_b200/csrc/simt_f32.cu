@@ -1,0 +1,264 @@
+// Exact fp32-in / fp32-out mode for the three fused programs.
+//
+// The north star requires fp32 inputs to match the float64 reference within
+// 1e-4, which TF32 tensor cores (10-bit mantissa) cannot meet, so this mode
+// runs on the FP32 FMA pipes. Each pattern is still one fused pass per tile:
+// row statistics are folded into the same K loop that feeds the contraction
+// (rules R4/R5: scale and shift applied after the dot), so no normalized
+// activations are materialized.
+//
+//   K1: gate/up tile kernel (stats + two contractions + SwiGLU -> H fp32),
+//       then the down contraction (snapshot-1 form; H in the workspace).
+//   K2: one kernel: X Yt^T plus sum(x), sum(x^2), colsum(Yt) in the K loop.
+//   K3: online-softmax attention, one CTA per (head, 16 query rows).
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+
+namespace bfgpu {
+
+extern void note_launch();
+
+namespace simt {
+
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256;
+
+enum Epi : int { kPlain = 0, kSwiGLU = 1, kLNMM = 2 };
+
+struct EpiParams {
+  float inv_k;  // 1/total(K) of the normalized operand
+  float eps;
+};
+
+// C[M,N] = epilogue(A[M,K] . B[N,K]^T (, A . B2^T)), all row-major fp32.
+template <int EPI>
+__global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                           const float* __restrict__ B2, float* __restrict__ C, int M,
+                                                           int N, int K, EpiParams ep) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  __shared__ float B2s[EPI == kSwiGLU ? BK : 1][BN + 4];
+  __shared__ float row_s1[BM], row_s2[BM], col_s[BN];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+  float acc[4][4] = {};
+  float acc2[4][4] = {};
+  float s1 = 0.f, s2 = 0.f, cs = 0.f;  // stats owned by threads < 64 (rows) and 64..127 (cols)
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    for (int i = tid; i < BM * BK; i += THREADS) {
+      const int r = i / BK, c = i % BK;
+      const int gm = m0 + r, gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? A[static_cast<size_t>(gm) * K + gk] : 0.f;
+      const int gn = n0 + r;
+      Bs[c][r] = (gn < N && gk < K) ? B[static_cast<size_t>(gn) * K + gk] : 0.f;
+      if constexpr (EPI == kSwiGLU) B2s[c][r] = (gn < N && gk < K) ? B2[static_cast<size_t>(gn) * K + gk] : 0.f;
+    }
+    __syncthreads();
+    if constexpr (EPI != kPlain) {
+      if (tid < BM) {
+#pragma unroll
+        for (int c = 0; c < BK; ++c) {
+          const float x = As[c][tid];
+          s1 += x;
+          s2 = fmaf(x, x, s2);
+        }
+      } else if (EPI == kLNMM && tid < BM + BN) {
+#pragma unroll
+        for (int c = 0; c < BK; ++c) cs += Bs[c][tid - BM];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < BK; ++c) {
+      float a[4], b[4], b2[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[c][ty * 4 + i];
+        b[i] = Bs[c][tx * 4 + i];
+        if constexpr (EPI == kSwiGLU) b2[i] = B2s[c][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          if constexpr (EPI == kSwiGLU) acc2[i][j] = fmaf(a[i], b2[j], acc2[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+  if constexpr (EPI != kPlain) {
+    if (tid < BM) {
+      row_s1[tid] = s1;
+      row_s2[tid] = s2;
+    } else if (EPI == kLNMM && tid < BM + BN) {
+      col_s[tid - BM] = cs;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i, gm = m0 + r;
+    if (gm >= M) continue;
+    float scale = 1.f, mu = 0.f;
+    if constexpr (EPI == kSwiGLU) scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k + ep.eps);
+    if constexpr (EPI == kLNMM) {
+      mu = row_s1[r] * ep.inv_k;
+      // var = t2/total(K) + (0 - square(t1/total(K)))   (fused program)
+      scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k - mu * mu + ep.eps);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = tx * 4 + j, gn = n0 + c;
+      if (gn >= N) continue;
+      float v = acc[i][j];
+      if constexpr (EPI == kSwiGLU) {
+        const float g = scale * v, u = scale * acc2[i][j];
+        v = g / (1.0f + expf(-g)) * u;
+      } else if constexpr (EPI == kLNMM) {
+        v = (v - mu * col_s[c]) * scale;
+      }
+      C[static_cast<size_t>(gm) * N + gn] = v;
+    }
+  }
+}
+
+// Online-softmax attention, fp32. One CTA = 16 query rows of one head.
+constexpr int AQ = 16, AKV = 64, ATHREADS = 128, AMAXD = 256;
+
+__global__ void __launch_bounds__(ATHREADS) attn_f32_kernel(const float* __restrict__ Q, const float* __restrict__ Kx,
+                                                            const float* __restrict__ Vt, float* __restrict__ O,
+                                                            int Sq, int Skv, int D, int Dv, float scale) {
+  __shared__ float q_s[AQ][AMAXD];
+  __shared__ float s_s[AQ][AKV + 1];
+  __shared__ float row_m[AQ], row_l[AQ], row_alpha[AQ];
+  const int h = blockIdx.y;
+  const int q0 = blockIdx.x * AQ;
+  const float* Qh = Q + static_cast<size_t>(h) * Sq * D;
+  const float* Kh = Kx + static_cast<size_t>(h) * Skv * D;
+  const float* Vh = Vt + static_cast<size_t>(h) * Dv * Skv;
+  float* Oh = O + static_cast<size_t>(h) * Sq * Dv;
+  const int tid = threadIdx.x;
+
+  for (int i = tid; i < AQ * D; i += ATHREADS) {
+    const int r = i / D, c = i % D;
+    q_s[r][c] = (q0 + r < Sq) ? Qh[static_cast<size_t>(q0 + r) * D + c] : 0.f;
+  }
+  if (tid < AQ) {
+    row_m[tid] = -INFINITY;
+    row_l[tid] = 0.f;
+  }
+  // each thread owns output elements (r, c) with idx = tid + k*ATHREADS over AQ*Dv
+  constexpr int MAXO = AQ * AMAXD / ATHREADS;
+  float o_acc[MAXO];
+#pragma unroll
+  for (int i = 0; i < MAXO; ++i) o_acc[i] = 0.f;
+  __syncthreads();
+
+  for (int n0 = 0; n0 < Skv; n0 += AKV) {
+    // S = scale * Q K^T for this key block
+    for (int i = tid; i < AQ * AKV; i += ATHREADS) {
+      const int r = i / AKV, c = i % AKV;
+      float s = -INFINITY;
+      if (n0 + c < Skv) {
+        const float* kr = Kh + static_cast<size_t>(n0 + c) * D;
+        float a = 0.f;
+        for (int d = 0; d < D; ++d) a = fmaf(q_s[r][d], kr[d], a);
+        s = a * scale;
+      }
+      s_s[r][c] = s;
+    }
+    __syncthreads();
+    // row-wise rebase (safe_attention_rows, safe_numerics.hpp:158-170)
+    if (tid < AQ) {
+      float mx = row_m[tid];
+      for (int c = 0; c < AKV; ++c) mx = fmaxf(mx, s_s[tid][c]);
+      const float alpha = (row_m[tid] == -INFINITY) ? 0.f : expf(row_m[tid] - mx);
+      float l = 0.f;
+      for (int c = 0; c < AKV; ++c) {
+        const float e = (s_s[tid][c] == -INFINITY) ? 0.f : expf(s_s[tid][c] - mx);
+        s_s[tid][c] = e;
+        l += e;
+      }
+      row_l[tid] = row_l[tid] * alpha + l;
+      row_m[tid] = mx;
+      row_alpha[tid] = alpha;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MAXO; ++i) {
+      const int idx = tid + i * ATHREADS;
+      if (idx >= AQ * Dv) break;
+      const int r = idx / Dv, c = idx % Dv;
+      const float* vr = Vh + static_cast<size_t>(c) * Skv + n0;
+      float a = 0.f;
+      const int nvalid = min(AKV, Skv - n0);
+      for (int j = 0; j < nvalid; ++j) a = fmaf(s_s[r][j], vr[j], a);
+      o_acc[i] = o_acc[i] * row_alpha[r] + a;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < MAXO; ++i) {
+    const int idx = tid + i * ATHREADS;
+    if (idx >= AQ * Dv) break;
+    const int r = idx / Dv, c = idx % Dv;
+    if (q0 + r < Sq) Oh[static_cast<size_t>(q0 + r) * Dv + c] = o_acc[i] / row_l[r];
+  }
+}
+
+template <int EPI>
+void launch_gemm(const float* A, const float* B, const float* B2, float* C, int64_t M, int64_t N, int64_t K,
+                 EpiParams ep, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
+  BF_CHECK_ARG(grid.y <= 65535, "fp32 mode: M too large");
+  gemm_f32_kernel<EPI><<<grid, THREADS, 0, s>>>(A, B, B2, C, static_cast<int>(M), static_cast<int>(N),
+                                                 static_cast<int>(K), ep);
+  BF_CUDA(cudaGetLastError());
+  note_launch();
+}
+
+}  // namespace simt
+
+size_t ffn_f32_workspace_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 4, 256); }
+
+void ffn_swiglu_f32(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
+                    int64_t F, int64_t N, float eps, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  BF_CHECK_ARG(M > 0 && D > 0 && F > 0 && N > 0, "bf_rms_ffn_swiglu: sizes must be positive");
+  BF_CHECK_ARG(ws != nullptr && ws_bytes >= ffn_f32_workspace_bytes(M, F), "bf_rms_ffn_swiglu: workspace too small");
+  float* H = static_cast<float*>(ws);
+  simt::launch_gemm<simt::kSwiGLU>(static_cast<const float*>(X), static_cast<const float*>(Wt),
+                                   static_cast<const float*>(Vt), H, M, F, D, {1.0f / static_cast<float>(D), eps},
+                                   stream);
+  simt::launch_gemm<simt::kPlain>(H, static_cast<const float*>(Ut), nullptr, static_cast<float*>(O), M, N, F,
+                                  {0.f, 0.f}, stream);
+}
+
+void lnmm_f32(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
+              size_t ws_bytes, cudaStream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  BF_CHECK_ARG(M > 0 && K > 0 && N > 0, "bf_layernorm_matmul: sizes must be positive");
+  simt::launch_gemm<simt::kLNMM>(static_cast<const float*>(X), static_cast<const float*>(Yt), nullptr,
+                                 static_cast<float*>(O), M, N, K, {1.0f / static_cast<float>(K), eps}, stream);
+}
+
+void attention_f32(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
+                   int64_t D, int64_t Dv, float scale, cudaStream_t stream) {
+  BF_CHECK_ARG(BH > 0 && Sq > 0 && Skv > 0 && D > 0 && Dv > 0, "bf_attention: sizes must be positive");
+  BF_CHECK_ARG(D <= simt::AMAXD && Dv <= simt::AMAXD, "bf_attention: fp32 mode supports D, Dv <= 256");
+  BF_CHECK_ARG(BH <= 65535, "bf_attention: too many heads for one launch");
+  if (scale <= 0.f) scale = 1.0f / sqrtf(static_cast<float>(D));
+  dim3 grid(static_cast<unsigned>((Sq + simt::AQ - 1) / simt::AQ), static_cast<unsigned>(BH));
+  simt::attn_f32_kernel<<<grid, simt::ATHREADS, 0, stream>>>(
+      static_cast<const float*>(Q), static_cast<const float*>(K), static_cast<const float*>(Vt),
+      static_cast<float*>(O), static_cast<int>(Sq), static_cast<int>(Skv), static_cast<int>(D), static_cast<int>(Dv),
+      scale);
+  BF_CUDA(cudaGetLastError());
+  note_launch();
+}
+
+}  // namespace bfgpu

@@ -1,0 +1,139 @@
+"""Torch-tensor front end over the C-ABI (device memory and streams only).
+
+PyTorch is plumbing here: it owns the device buffers and the current stream.
+All arithmetic happens in libbfgpu.so kernels. Every function validates
+shapes/dtypes and raises BfError with the library's message on failure.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import BF_DTYPE_BF16, BF_DTYPE_F32, BF_FFN_FUSED, BF_FFN_TWO_PHASE, check
+
+_WS: dict[int, torch.Tensor] = {}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF_DTYPE_BF16
+    if t.dtype == torch.float32:
+        return BF_DTYPE_F32
+    raise TypeError(f"unsupported dtype {t.dtype}; expected bfloat16 or float32")
+
+
+def _require(t: torch.Tensor, name: str, shape: tuple, dtype: torch.dtype, device) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major)")
+
+
+def _workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    ws = _WS.get(idx)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[idx] = ws
+    return ws
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def rms_ffn_swiglu(X, Wt, Vt, Ut, eps: float = 0.0, schedule: str = "fused", out=None, workspace=None):
+    """O = (swish(r*X Wt^T) * (r*X Vt^T)) Ut^T with r = 1/sqrt(mean(X^2) + eps).
+
+    Mirrors ref::rms_ffn_swiglu (interpreter.hpp:553-559): X[M,D], Wt/Vt[F,D],
+    Ut[N,F] ("transposed" right operands, lowering.hpp:583-597).
+    """
+    M, D = X.shape
+    F = Wt.shape[0]
+    N = Ut.shape[0]
+    dt = X.dtype
+    dev = X.device
+    _require(X, "X", (M, D), dt, dev)
+    _require(Wt, "Wt", (F, D), dt, dev)
+    _require(Vt, "Vt", (F, D), dt, dev)
+    _require(Ut, "Ut", (N, F), dt, dev)
+    sched = {"fused": BF_FFN_FUSED, "two_phase": BF_FFN_TWO_PHASE}[schedule]
+    if out is None:
+        out = torch.empty((M, N), dtype=dt, device=dev)
+    _require(out, "out", (M, N), dt, dev)
+    code = _dtype_code(X)
+    L = _lib.lib()
+    nbytes = L.bf_rms_ffn_swiglu_workspace_bytes(M, D, F, N, code, sched)
+    ws = workspace if workspace is not None else _workspace(nbytes, dev)
+    check(
+        L.bf_rms_ffn_swiglu(
+            X.data_ptr(), Wt.data_ptr(), Vt.data_ptr(), Ut.data_ptr(), out.data_ptr(), M, D, F, N, code,
+            float(eps), sched, ws.data_ptr(), ws.numel(), _stream_ptr(dev),
+        )
+    )
+    return out
+
+
+def layernorm_matmul(X, Yt, eps: float = 0.0, out=None, workspace=None):
+    """O = layernorm(X) Yt^T without eps/gamma/beta (ref::layernorm_matmul, interpreter.hpp:549-551)."""
+    M, K = X.shape
+    N = Yt.shape[0]
+    dt = X.dtype
+    dev = X.device
+    _require(X, "X", (M, K), dt, dev)
+    _require(Yt, "Yt", (N, K), dt, dev)
+    if out is None:
+        out = torch.empty((M, N), dtype=dt, device=dev)
+    _require(out, "out", (M, N), dt, dev)
+    code = _dtype_code(X)
+    L = _lib.lib()
+    nbytes = L.bf_layernorm_matmul_workspace_bytes(M, K, N, code)
+    ws = workspace if workspace is not None else _workspace(nbytes, dev)
+    check(
+        L.bf_layernorm_matmul(
+            X.data_ptr(), Yt.data_ptr(), out.data_ptr(), M, K, N, code, float(eps), ws.data_ptr(), ws.numel(),
+            _stream_ptr(dev),
+        )
+    )
+    return out
+
+
+def attention(Q, K, Vt, scale: float | None = None, out=None):
+    """O = softmax(scale Q K^T) V with V given as Vt (ref::attention, interpreter.hpp:543-547).
+
+    Q: [..., Sq, D], K: [..., Skv, D], Vt: [..., Dv, Skv]; leading dims are heads.
+    """
+    *lead, Sq, D = Q.shape
+    Skv = K.shape[-2]
+    Dv = Vt.shape[-2]
+    BH = 1
+    for x in lead:
+        BH *= x
+    dt = Q.dtype
+    dev = Q.device
+    _require(Q, "Q", (*lead, Sq, D), dt, dev)
+    _require(K, "K", (*lead, Skv, D), dt, dev)
+    _require(Vt, "Vt", (*lead, Dv, Skv), dt, dev)
+    if out is None:
+        out = torch.empty((*lead, Sq, Dv), dtype=dt, device=dev)
+    _require(out, "out", (*lead, Sq, Dv), dt, dev)
+    L = _lib.lib()
+    check(
+        L.bf_attention(
+            Q.data_ptr(), K.data_ptr(), Vt.data_ptr(), out.data_ptr(), BH, Sq, Skv, D, Dv, _dtype_code(Q),
+            float(scale) if scale is not None else 0.0, _stream_ptr(dev),
+        )
+    )
+    return out
+
+
+def kernel_launches() -> int:
+    return int(_lib.lib().bf_kernel_launches())
