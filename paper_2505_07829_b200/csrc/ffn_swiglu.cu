@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t row = q * 32 + lane;
     const bool leader = threadIdx.x == 4 * 32;
     uint32_t acc = 0, aphase = 0;
-    uint32_t sphase[2] = {0, 0};  // sfull[a] completes once per gate/up tile on slot a
+    uint32_t sphase = 0;  // bit a: parity of sfull[a], which completes once per gate/up tile on slot a
     const uint32_t out_addr = smem_u32(out_stage);
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       const Tile tl = decode_tile(p, t);
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const uint32_t trow = tmem_base + acc * 256 + ((q * 32) << 16);
       if (tl.kind == 0) {
-        mbar_wait(&sfull[acc], sphase[acc]);
-        sphase[acc] ^= 1;
+        mbar_wait(&sfull[acc], (sphase >> acc) & 1u);
+        sphase ^= 1u << acc;
         const float r = rstat[acc * BM + row];
         if (leader) bulk_wait_read0();  // staging buffer free again
         named_bar_sync(1, EPI_THREADS);

@@ -46,6 +46,23 @@ inline CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dtype, uin
   return m;
 }
 
+// [batch, rows, cols] bf16 tensor, contiguous; box = box_cols x box_rows x 1, 128-byte swizzle.
+// Out-of-bounds handling is per batch entry (a row tile never spills into the next head).
+inline CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t batch, uint64_t rows, uint64_t cols,
+                                     uint32_t box_cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cols, rows, batch};
+  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (3d) failed (code " + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 inline CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_cols,
                                   uint32_t box_rows) {
   return make_tmap_2d(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, ld, box_cols, box_rows);

@@ -1,0 +1,58 @@
+"""Shared test helpers: golden fixtures, bf16 rounding, and the parity metrics.
+
+Tolerances (BASELINE.json north_star): bf16 inputs with fp32 accumulation must
+match the float64 reference within max relative error 2e-2 (max|d| / max|ref|)
+and max abs error 1e-2 on normalized outputs (|d| / rms(ref)); fp32-in/fp32-out
+must match within 1e-4 (max|d| / max|ref|). The reference's own
+max_rel_error (interpreter.hpp:599-610, 1e-12 absolute floor) is meaningless
+for bf16, so these metrics are stated here and used by every parity test.
+"""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+BF16_REL_TOL = 2e-2
+BF16_NORM_ABS_TOL = 1e-2
+F32_REL_TOL = 1e-4
+
+
+def golden(name: str) -> dict:
+    with np.load(GOLDEN / f"{name}.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    f = np.asarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def rel_err(out, ref) -> float:
+    out = np.asarray(out, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(out - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def norm_abs_err(out, ref) -> float:
+    out = np.asarray(out, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    rms = float(np.sqrt(np.mean(ref * ref)))
+    return float(np.max(np.abs(out - ref)) / max(rms, 1e-300))
+
+
+def assert_bf16_close(out, ref, what: str = "", norm_tol: float = BF16_NORM_ABS_TOL) -> None:
+    assert np.all(np.isfinite(out)), f"{what}: non-finite output"
+    r, n = rel_err(out, ref), norm_abs_err(out, ref)
+    assert r <= BF16_REL_TOL, f"{what}: max|d|/max|ref| = {r:.3e} > {BF16_REL_TOL}"
+    assert n <= norm_tol, f"{what}: max|d|/rms(ref) = {n:.3e} > {norm_tol}"
+
+
+def assert_f32_close(out, ref, what: str = "") -> None:
+    assert np.all(np.isfinite(out)), f"{what}: non-finite output"
+    r = rel_err(out, ref)
+    assert r <= F32_REL_TOL, f"{what}: max|d|/max|ref| = {r:.3e} > {F32_REL_TOL}"
