@@ -86,16 +86,25 @@ DimBinding parse_binding(const char* spec) {
   return b;
 }
 
+// Row-major <-> column-major conversion, tiled so both sides stay in cache
+// (these are wrapper costs, kept out of the reference's own timing as far as possible).
 Matrix from_rowmajor(const double* p, long rows, long cols) {
   Matrix m(rows, cols);
-  for (long i = 0; i < rows; ++i)
-    for (long j = 0; j < cols; ++j) m(i, j) = p[i * cols + j];
+  constexpr long TB = 64;
+  for (long i0 = 0; i0 < rows; i0 += TB)
+    for (long j0 = 0; j0 < cols; j0 += TB)
+      for (long j = j0; j < std::min(cols, j0 + TB); ++j)
+        for (long i = i0; i < std::min(rows, i0 + TB); ++i) m(i, j) = p[i * cols + j];
   return m;
 }
 
 void to_rowmajor(const Matrix& m, double* p) {
-  for (long i = 0; i < m.rows(); ++i)
-    for (long j = 0; j < m.cols(); ++j) p[i * m.cols() + j] = m(i, j);
+  constexpr long TB = 64;
+  const long rows = m.rows(), cols = m.cols();
+  for (long i0 = 0; i0 < rows; i0 += TB)
+    for (long j0 = 0; j0 < cols; j0 += TB)
+      for (long i = i0; i < std::min(rows, i0 + TB); ++i)
+        for (long j = j0; j < std::min(cols, j0 + TB); ++j) p[i * cols + j] = m(i, j);
 }
 
 template <class Fn>

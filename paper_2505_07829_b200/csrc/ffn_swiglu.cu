@@ -345,6 +345,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ss1 = fmaf(hi, hi, ss1);
             }
           }
+          // Shared loads must have completed before the slot is released: the mbarrier
+          // arrive does not wait for outstanding LDS, so a TMA refill could overwrite
+          // the stage under an in-flight load (observed as run-to-run stats drift).
+          __threadfence_block();
           mbar_arrive(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -353,6 +357,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         mbar_wait(&tempty[acc], aphase ^ 1);
         rstat[acc * BM + row] = 1.0f / sqrtf((ss0 + ss1) * p.inv_d + p.eps);
+        __threadfence_block();  // publish the STS before the arrive (SYNCS does not order it)
         mbar_arrive(&sfull[acc]);
       } else {
         // Down tiles carry no statistics, but the stats warps still consume every

@@ -293,6 +293,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             s2b = fmaf(hi, hi, s2b);
           }
         }
+        // Shared loads must have completed before the slot is released: the mbarrier
+        // arrive does not wait for outstanding LDS, so a TMA refill could overwrite
+        // the stage under an in-flight load (observed as run-to-run stats drift).
+        __threadfence_block();
         mbar_arrive(&empty[stage]);
         if (++stage == STAGES) {
           stage = 0;
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const float var = (s2a + s2b) * p.inv_k - mean * mean + p.eps;
       s_mu[acc * BM + row] = -mean;
       s_rstd[acc * BM + row] = 1.0f / sqrtf(var);
+      __threadfence_block();  // publish the STS before the arrive (SYNCS does not order it)
       mbar_arrive(&sfull[acc]);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
