@@ -62,6 +62,14 @@ def lib():
         ]
         l.bfref_safe_attention.argtypes = [_dp, _dp, _dp, ctypes.c_long, ctypes.c_long, ctypes.c_long, ctypes.c_long,
                                            ctypes.c_int, _dp]
+        l.bfref_session_create.restype = ctypes.c_void_p
+        l.bfref_session_create.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+            ctypes.POINTER(_dp), ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long), ctypes.c_long,
+            ctypes.c_long, ctypes.c_int,
+        ]
+        l.bfref_session_step.argtypes = [ctypes.c_void_p, _dp, _dp]
+        l.bfref_session_destroy.argtypes = [ctypes.c_void_p]
         _lib = l
     return _lib
 
@@ -183,3 +191,39 @@ def safe_attention(q: np.ndarray, k: np.ndarray, vt: np.ndarray, row_chunks: int
     _check(lib().bfref_safe_attention(qp, kp, vp, q.shape[0], k.shape[0], q.shape[1], vt.shape[0], row_chunks,
                                       out.ctypes.data_as(_dp)))
     return out
+
+
+class Session:
+    """Row-sharded reference executor: `workers` threads, each running
+    blockfuse::execute on its own `shard_rows`-row shard per step. The shared
+    operands (weights) are converted once here, outside any timed region."""
+
+    def __init__(self, which: int, snap: int, shared: dict[str, np.ndarray], row_name: str, row_cols: int,
+                 out_cols: int, shard_binding: dict, shard_rows: int, workers: int):
+        order = [row_name] + [n for n in INPUTS[which] if n != row_name]
+        dummy = np.zeros((1, row_cols))
+        arrays = {row_name: dummy, **shared}
+        keep, names, data, rows, cols = _pack_inputs(arrays, order)
+        self.workers = workers
+        self.shard_rows = shard_rows
+        self.out_cols = out_cols
+        self._h = lib().bfref_session_create(which, snap, binding_str(shard_binding), len(order), names, data, rows,
+                                             cols, shard_rows, out_cols, workers)
+        del keep
+        if not self._h:
+            _check(1)
+
+    def step(self, rows: np.ndarray) -> np.ndarray:
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        assert rows.shape[0] == self.workers * self.shard_rows
+        out = np.zeros((rows.shape[0], self.out_cols))
+        _check(lib().bfref_session_step(self._h, rows.ctypes.data_as(_dp), out.ctypes.data_as(_dp)))
+        return out
+
+    def close(self) -> None:
+        if self._h:
+            lib().bfref_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
