@@ -407,6 +407,8 @@ def run_ours(args, wl):
         kernel_ms = ms_per_step  # one fused launch per step (fused schedule); per-rank device time
         achieved = inp["flops"] / (max_elapsed_ms / args.steps / 1e3) / 1e12
         kkey = {"ffn": "ffn_swiglu_kernel", "lnmm": "ln_matmul_kernel", "attn": "attn_kernel"}[kind]
+        capture = {"ffn": "prof_ffn" if args.schedule == "fused" else "prof_ffn2p", "lnmm": "prof_lnmm",
+                   "attn": "prof_attn"}[kind]
         line = {
             "metric": METRIC,
             "value": value,
@@ -429,13 +431,13 @@ def run_ours(args, wl):
                 "bound": "tensor", "achieved": achieved, "peak": peaks.get("bf16_tflops"), "unit": "TFLOP/s",
                 "frac": achieved / peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]),
                 "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]),
-                "peak_source": peaks_src + ", cuBLAS bf16 burst", "traffic": ncu_traffic(kkey),
+                "peak_source": peaks_src + ", cuBLAS bf16 burst", "traffic": ncu_traffic(f"{kkey}@{capture}"),
                 "kernel": kkey, "flops_per_launch": inp["flops"], "ms_per_launch": kernel_ms,
             },
             "hbm_bytes": {
                 "fused_algorithmic_per_gpu": inp["fused_bytes"], "unfused_op_sequence_per_gpu": inp["unfused_bytes"],
                 "unfused_over_fused": inp["unfused_bytes"] / inp["fused_bytes"], "reference_model": model,
-                "measured_ncu_per_launch": ncu_traffic(kkey),
+                "measured_ncu_per_launch": ncu_traffic(f"{kkey}@{capture}"),
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -107,6 +107,17 @@ BF_API int bf_attention(const void* Q, const void* K, const void* Vt, void* O, i
                  int64_t D, int64_t Dv, int dtype, float scale, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Device memory helpers for host bindings that do not own a CUDA runtime
+ * (the C++ execute() adapter, cgo/JNI-style callers). Thin wrappers over the
+ * CUDA runtime; the copies are stream-ordered and asynchronous for pinned memory.
+ * ---------------------------------------------------------------------- */
+BF_API void* bf_device_alloc(size_t bytes);
+BF_API int bf_device_free(void* ptr);
+BF_API int bf_copy_to_device(void* dst, const void* src, size_t bytes, void* stream);
+BF_API int bf_copy_to_host(void* dst, const void* src, size_t bytes, void* stream);
+BF_API int bf_stream_synchronize(void* stream);
+
+/* ------------------------------------------------------------------------
  * Introspection
  * ---------------------------------------------------------------------- */
 BF_API const char* bf_last_error(void);

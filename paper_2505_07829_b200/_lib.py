@@ -48,6 +48,11 @@ _SIGNATURES = [
         ctypes.c_int,
         [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, _vp],
     ),
+    ("bf_device_alloc", ctypes.c_void_p, [ctypes.c_size_t]),
+    ("bf_device_free", ctypes.c_int, [_vp]),
+    ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
+    ("bf_copy_to_host", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
+    ("bf_stream_synchronize", ctypes.c_int, [_vp]),
     ("bf_last_error", ctypes.c_char_p, []),
     ("bf_version", ctypes.c_int, []),
     ("bf_kernel_launches", ctypes.c_uint64, []),

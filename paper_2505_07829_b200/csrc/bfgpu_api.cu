@@ -140,4 +140,30 @@ int bf_attention(const void* Q, const void* K, const void* Vt, void* O, int64_t 
   });
 }
 
+void* bf_device_alloc(size_t bytes) {
+  void* p = nullptr;
+  const int rc = guarded([&] { BF_CUDA(cudaMalloc(&p, bytes ? bytes : 1)); });
+  return rc == BF_OK ? p : nullptr;
+}
+
+int bf_device_free(void* ptr) {
+  return guarded([&] { BF_CUDA(cudaFree(ptr)); });
+}
+
+int bf_copy_to_device(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] {
+    BF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int bf_copy_to_host(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] {
+    BF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int bf_stream_synchronize(void* stream) {
+  return guarded([&] { BF_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+}
+
 }  // extern "C"

@@ -1,0 +1,12 @@
+#!/bin/bash
+# One GPU session: smoke, bench line, launch list, full ncu capture of the top kernel.
+set -x
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 2 -c 1 -o gpurun_out/prof_ffn -f python scripts/ncu_target.py ffn_8b fused 3 > gpurun_out/ncu_ffn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 4 -c 2 -o gpurun_out/prof_ffn2p -f python scripts/ncu_target.py ffn_8b two_phase 3 > gpurun_out/ncu_ffn2p.log 2>&1
+timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
+lscpu > gpurun_out/lscpu.txt; free -g >> gpurun_out/lscpu.txt

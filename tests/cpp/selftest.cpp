@@ -1,0 +1,127 @@
+// TEST HARNESS — compares bfgpu::execute (the drop-in adapter, GPU) against
+// blockfuse::execute (the reference CPU executor) on the reference's own
+// programs and random_inputs, exposed as C for tests/test_execute_gpu.py.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "bfgpu_execute.hpp"
+#include "blockfuse/engine.hpp"
+#include "blockfuse/lowering.hpp"
+
+using namespace blockfuse;
+
+namespace {
+
+ArrayProgram example(int which, double eps) {
+  if (which == 0) return examples::attention();
+  if (which == 1) return examples::layernorm_matmul();
+  ArrayProgram p;  // examples::rms_ffn_swiglu with an explicit rmsnorm epsilon
+  NodeId x = p.input("X", "M", "D");
+  NodeId wt = p.input("Wt", "K", "D", true);
+  NodeId vt = p.input("Vt", "K", "D", true);
+  NodeId ut = p.input("Ut", "N", "K", true);
+  NodeId xn = p.op("rmsnorm", {x}, {}, eps);
+  NodeId a = p.op("matmul", {xn, wt});
+  NodeId b = p.op("matmul", {xn, vt});
+  NodeId h = p.op("hadamard", {p.op("swish", {a}), b});
+  p.output("O", p.op("matmul", {h, ut}));
+  return p;
+}
+
+DimBinding parse(const char* spec) {
+  DimBinding b;
+  std::string s(spec);
+  size_t pos = 0;
+  while (pos < s.size()) {
+    size_t end = s.find(',', pos);
+    if (end == std::string::npos) end = s.size();
+    std::string item = s.substr(pos, end - pos);
+    auto eq = item.find('='), x = item.find('x');
+    b.dims[item.substr(0, eq)] = {std::stoi(item.substr(eq + 1, x - eq - 1)), std::stoi(item.substr(x + 1))};
+    pos = end + 1;
+  }
+  return b;
+}
+
+double bf16_round(double v) {
+  float f = static_cast<float>(v);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+void set_msg(char* msg, int len, const std::string& s) {
+  if (msg && len > 0) {
+    std::strncpy(msg, s.c_str(), static_cast<size_t>(len - 1));
+    msg[len - 1] = 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// snap: fusion snapshot index, -1 final, -2 the unfused lower() program (must be rejected).
+__attribute__((visibility("default"))) int bfx_compare(int which, int snap, const char* binding, int precision,
+                                                       unsigned long long seed, double eps, double* rel_err,
+                                                       double* norm_err, int* pattern, int* rec_snapshot,
+                                                       char* msg, int msglen) {
+  try {
+    BlockGraph unfused = lower(example(which, eps));
+    FuseResult fr = fuse(unfused);
+    const BlockGraph& prog = snap == -2 ? unfused : (snap == -1 ? fr.snapshots.back().program : fr.snapshots.at(snap).program);
+    DimBinding b = parse(binding);
+    auto in = random_inputs(input_specs(unfused, b), seed);
+    if (precision == 0)
+      for (auto& [name, m] : in)
+        for (long i = 0; i < m.rows(); ++i)
+          for (long j = 0; j < m.cols(); ++j) m(i, j) = bf16_round(m(i, j));
+    bfgpu::Recognized r = bfgpu::recognize(prog);
+    *pattern = static_cast<int>(r.pattern);
+    *rec_snapshot = r.snapshot;
+    bfgpu::ExecConfig cfg;
+    cfg.precision = precision == 0 ? bfgpu::Precision::BF16 : bfgpu::Precision::F32;
+    auto got = bfgpu::execute(prog, in, b, cfg);
+    auto ref = execute(prog, in, b);  // the reference CPU executor on the same program and inputs
+    const Matrix& g = got.at("O");
+    const Matrix& e = ref.at("O");
+    double maxd = 0, maxr = 0, ss = 0;
+    for (long i = 0; i < e.rows(); ++i)
+      for (long j = 0; j < e.cols(); ++j) {
+        maxd = std::max(maxd, std::abs(g(i, j) - e(i, j)));
+        maxr = std::max(maxr, std::abs(e(i, j)));
+        ss += e(i, j) * e(i, j);
+      }
+    *rel_err = maxd / std::max(maxr, 1e-300);
+    *norm_err = maxd / std::max(std::sqrt(ss / static_cast<double>(e.size())), 1e-300);
+    set_msg(msg, msglen, "ok");
+    return 0;
+  } catch (const std::exception& ex) {
+    set_msg(msg, msglen, ex.what());
+    return 1;
+  }
+}
+
+__attribute__((visibility("default"))) int bfx_recognize(int which, int snap, double eps, int* pattern,
+                                                         int* rec_snapshot, double* eps_out, char* msg, int msglen) {
+  try {
+    BlockGraph unfused = lower(example(which, eps));
+    FuseResult fr = fuse(unfused);
+    const BlockGraph& prog = snap == -2 ? unfused : (snap == -1 ? fr.snapshots.back().program : fr.snapshots.at(snap).program);
+    bfgpu::Recognized r = bfgpu::recognize(prog);
+    *pattern = static_cast<int>(r.pattern);
+    *rec_snapshot = r.snapshot;
+    *eps_out = r.eps;
+    set_msg(msg, msglen, r.materializes_intermediate ? "materializes" : "fused");
+    return 0;
+  } catch (const std::exception& ex) {
+    set_msg(msg, msglen, ex.what());
+    return 1;
+  }
+}
+
+}  // extern "C"
