@@ -30,6 +30,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+from paper_2505_07829_b200.launcher import max_over_ranks, shard  # noqa: E402
+
 METRIC = "fused RMSNorm+SwiGLU-FFN TFLOP/s & % bf16 peak; HBM bytes vs unfused"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -152,7 +154,7 @@ def make_inputs(wl: dict, rank: int, world: int, device):
     g = torch.Generator(device=device)
     kind = wl["kind"]
     if kind == "ffn":
-        rows = wl.get("rows_per_rank") or wl["rows_total"] // world
+        rows = wl.get("rows_per_rank") or shard(wl["rows_total"], rank, world, 128).size
         D, F, N = wl["D"], wl["F"], wl["N"]
         g.manual_seed(1234)  # weights identical on every rank (no broadcast needed)
         Wt = (torch.randn(F, D, device=device, generator=g) * D ** -0.5).bfloat16()
@@ -164,7 +166,7 @@ def make_inputs(wl: dict, rank: int, world: int, device):
         fused, unfused = ffn_bytes(rows, D, F, N)
         return dict(X=X, Wt=Wt, Vt=Vt, Ut=Ut, rows=rows, flops=flops, fused_bytes=fused, unfused_bytes=unfused)
     if kind == "lnmm":
-        rows = wl["rows_total"] // world
+        rows = shard(wl["rows_total"], rank, world, 128).size
         K, N = wl["K"], wl["N"]
         g.manual_seed(1234)
         Yt = torch.randn(N, K, device=device, generator=g).bfloat16()
@@ -173,13 +175,24 @@ def make_inputs(wl: dict, rank: int, world: int, device):
         return dict(X=X, Yt=Yt, rows=rows, flops=2.0 * rows * K * N, fused_bytes=2 * (rows * K + N * K + rows * N),
                     unfused_bytes=2 * (rows * K * 2 + rows * K + N * K + rows * N))
     B, H, S, Dh = wl["B"], wl["H"], wl["S"], wl["Dh"]
-    heads = B * H // world
+    heads = shard(B * H, rank, world).size
     g.manual_seed(3000 + rank)
     Q = torch.randn(heads, S, Dh, device=device, generator=g).bfloat16()
     K = torch.randn(heads, S, Dh, device=device, generator=g).bfloat16()
     Vt = torch.randn(heads, Dh, S, device=device, generator=g).bfloat16()
     return dict(Q=Q, K=K, Vt=Vt, rows=heads, flops=4.0 * heads * S * S * Dh,
                 fused_bytes=2 * 4 * heads * S * Dh, unfused_bytes=2 * heads * (4 * S * Dh + 3 * S * S))
+
+
+def sum_over_ranks(value: float, device) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def step_fn(wl, inp, schedule, out):
@@ -337,12 +350,10 @@ def run_ours(args, wl):
     launches = ops.kernel_launches() - launches0
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     elapsed = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_elapsed_ms = t.item()
+    max_elapsed_ms = max_over_ranks(elapsed, dev)
     ms_per_step = max_elapsed_ms / args.steps
-    total_flops = inp["flops"] * world
+    # whole-job work: every rank's units (weak scaling: world x rows_per_rank)
+    total_flops = sum_over_ranks(inp["flops"], dev)
     value = total_flops / (ms_per_step / 1e3) / 1e12
 
     # ---- end to end through the public API with pinned host buffers (e2e)
@@ -374,10 +385,7 @@ def run_ours(args, wl):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = te.item() / e2e_steps
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev) / e2e_steps
     e2e_value = total_flops / (e2e_ms / 1e3) / 1e12
 
     # ---- reference-model traffic (the reference's own traffic_bytes, metrics.hpp:154)
