@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "sm100.cuh"
@@ -439,7 +440,18 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   p.inv_d = 1.0f / static_cast<float>(D);
   p.eps = eps;
   p.flags = flags;
-  p.group = 8;
+  // m-tiles per scheduling group: larger groups re-read the weights fewer times,
+  // smaller groups keep the live part of H small enough to stay in L2.
+  static const int group_env = [] {
+    const char* v = std::getenv("BFGPU_FFN_GROUP");
+    return v ? std::atoi(v) : 0;
+  }();
+  // Default: about 120 MB of H per group (32 m-tiles at ffn=14336, 16 at ffn=28672),
+  // measured best at the Llama-3-8B shape (g=8: 1226, g=16: 1304, g=32: 1417, g=64: 1251 TFLOP/s).
+  int g = static_cast<int>((120ll << 20) / (static_cast<long long>(BM) * F * 2));
+  int g2 = 4;
+  while (g2 * 2 <= g && g2 < 64) g2 *= 2;
+  p.group = group_env > 0 ? group_env : std::min(g2, p.Mt);
 
   const int dev = current_device();
   const int sms = num_sms(dev);
