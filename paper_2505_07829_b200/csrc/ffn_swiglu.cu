@@ -35,6 +35,7 @@
 #include "common.hpp"
 #include "sm100.cuh"
 #include "tma_host.hpp"
+#include "ffn_common.cuh"
 
 namespace bfgpu {
 namespace ffn {
@@ -55,59 +56,6 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t IDESC = dev::idesc_bf16_f32(128, 256);
 
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OUT_BYTES + 2 * BM * 4 /*rstat*/ + 256 /*barriers*/ + 1024;
-
-enum Mode : int { kFused = 0, kGateUpOnly = 1, kDownOnly = 2 };
-
-struct Params {
-  int M, D, F, N;
-  int Mt, Ft, Nt;
-  int group;
-  int mode;
-  int num_tiles;
-  int kt_d, kt_f;  // k-steps of 64 over D and over F
-  float inv_d;
-  float eps;
-  int* flags;      // per m-tile count of finished gate/up tiles (fused mode)
-};
-
-struct Tile {
-  int kind;  // 0 gate/up, 1 down
-  int m;     // m-tile
-  int j;     // f-chunk (kind 0) or n-chunk (kind 1)
-};
-
-__device__ __forceinline__ int group_size(const Params& p, int g) { return min(p.group, p.Mt - g * p.group); }
-
-// Linear tile index -> tile. Segments: fused  A0 A1 B0 A2 B1 ... A(G-1) B(G-2) B(G-1)
-//                                      gate/up-only A0 A1 ...; down-only B0 B1 ...
-__device__ Tile decode_tile(const Params& p, int t) {
-  const int ngroups = (p.Mt + p.group - 1) / p.group;
-  const int nseg = p.mode == kFused ? 2 * ngroups : ngroups;
-  for (int s = 0; s < nseg; ++s) {
-    int kind, g;
-    if (p.mode == kGateUpOnly) {
-      kind = 0;
-      g = s;
-    } else if (p.mode == kDownOnly) {
-      kind = 1;
-      g = s;
-    } else if (s == 0) {
-      kind = 0;
-      g = 0;
-    } else if (s == nseg - 1) {
-      kind = 1;
-      g = ngroups - 1;
-    } else {
-      kind = (s & 1) ? 0 : 1;
-      g = (s & 1) ? (s + 1) / 2 : s / 2 - 1;
-    }
-    const int gs = group_size(p, g);
-    const int cnt = gs * (kind == 0 ? p.Ft : p.Nt);
-    if (t < cnt) return Tile{kind, g * p.group + t % gs, t / gs};
-    t -= cnt;
-  }
-  return Tile{-1, 0, 0};
-}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ffn_swiglu_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wt,
@@ -393,17 +341,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 namespace {
 
 size_t ffn_h_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 2, 1024); }
-size_t ffn_flag_bytes(int64_t M) { return align_up(static_cast<size_t>((M + 127) / 128) * 4, 256); }
+size_t ffn_flag_bytes(int64_t M) { return align_up(static_cast<size_t>((M + 127) / 128 + 2) * 4, 256); }
+size_t ffn_rstat_bytes(int64_t M) { return align_up(static_cast<size_t>(M) * 4, 256); }
 
 }  // namespace
 
 size_t ffn_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
   (void)D;
   (void)N;
-  return ffn_h_bytes(M, F) + ffn_flag_bytes(M);
+  return ffn_h_bytes(M, F) + ffn_rstat_bytes(M) + ffn_flag_bytes(M);
 }
 
 extern void note_launch();
+void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, const CUtensorMap& tm_vt,
+                         const CUtensorMap& tm_ut_half, const CUtensorMap& tm_h, const CUtensorMap& tm_o,
+                         ffn::Params p, int schedule, int* flags, const void* X, float* rstat, int* stats_ready,
+                         cudaStream_t stream);
 
 void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
                      int64_t F, int64_t N, float eps, int schedule, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -418,7 +371,8 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
 
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   void* H = wsb;
-  int* flags = reinterpret_cast<int*>(wsb + ffn_h_bytes(M, F));
+  float* rstat = reinterpret_cast<float*>(wsb + ffn_h_bytes(M, F));
+  int* flags = reinterpret_cast<int*>(wsb + ffn_h_bytes(M, F) + ffn_rstat_bytes(M));
 
   const CUtensorMap tm_x = make_tmap_bf16(X, M, D, D, BK, BM);
   const CUtensorMap tm_wt = make_tmap_bf16(Wt, F, D, D, BK, BF);
@@ -452,6 +406,21 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   int g2 = 4;
   while (g2 * 2 <= g && g2 < 64) g2 *= 2;
   p.group = group_env > 0 ? group_env : std::min(g2, p.Mt);
+
+  // CTA-pair path (default): 256-row m-units, B split across the pair.
+  static const bool force_1sm = [] {
+    const char* v = std::getenv("BFGPU_FFN_1SM");
+    return v && v[0] == '1';
+  }();
+  if (!force_1sm) {
+    Params q = p;
+    q.Mt = static_cast<int>((M + 2 * BM - 1) / (2 * BM));
+    q.group = std::max(1, p.group / 2);
+    const CUtensorMap tm_ut_half = make_tmap_bf16(Ut, N, F, F, BK, 128);
+    ffn_swiglu_bf16_2sm(tm_x, tm_wt, tm_vt, tm_ut_half, tm_h, tm_o, q, schedule, flags, X, rstat,
+                        flags + q.Mt * 2, stream);
+    return;
+  }
 
   const int dev = current_device();
   const int sms = num_sms(dev);
