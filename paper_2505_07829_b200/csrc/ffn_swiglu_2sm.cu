@@ -199,22 +199,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int per = (p.M + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
       const int r0 = static_cast<int>(blockIdx.x) * per, r1 = min(p.M, r0 + per);
       for (int r = r0 + static_cast<int>(q); r < r1; r += 4) {
-        const uint4* rowp = reinterpret_cast<const uint4*>(ex.X + static_cast<size_t>(r) * p.D);
-        float s0 = 0.f, s1 = 0.f;
-        for (int c = lane; c < p.D / 8; c += 32) {
-          const uint4 v = __ldg(rowp + c);
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
-            s0 = fmaf(lo, lo, s0);
-            s1 = fmaf(hi, hi, s1);
-          }
-        }
-        float s = s0 + s1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) ex.rstat[r] = 1.0f / sqrtf(s * p.inv_d + p.eps);
+        const float2 mom = warp_row_moments_bf16(ex.X + static_cast<size_t>(r) * p.D, p.D, lane);
+        if (lane == 0) ex.rstat[r] = 1.0f / sqrtf(mom.y * p.inv_d + p.eps);
       }
       named_bar_sync(1, EPI_THREADS);
       if (store_leader) {

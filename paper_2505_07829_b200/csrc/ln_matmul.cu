@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "sm100.cuh"
@@ -328,11 +329,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 extern void note_launch();
 
+size_t lnmm2_workspace_bytes(int64_t M, int64_t N);
+void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
+                   size_t ws_bytes, cudaStream_t stream);
+
 size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype) {
-  (void)M;
   (void)K;
   if (dtype != BF_DTYPE_BF16) return 256;
-  return align_up(static_cast<size_t>(N) * 4, 256) + 256;
+  return std::max(align_up(static_cast<size_t>(N) * 4, 256) + 256, lnmm2_workspace_bytes(M, N));
 }
 
 void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
@@ -343,6 +347,15 @@ void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int
   BF_CHECK_ARG(M < (1ll << 31) && K < (1ll << 31) && N < (1ll << 31), "bf_layernorm_matmul: dimension too large");
   BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm_workspace_bytes(M, K, N, BF_DTYPE_BF16),
                "bf_layernorm_matmul: workspace too small");
+  // CTA-pair kernel by default; BFGPU_LNMM_1SM=1 selects the 1-SM kernel below.
+  static const bool force_1sm = [] {
+    const char* v = std::getenv("BFGPU_LNMM_1SM");
+    return v && v[0] == '1';
+  }();
+  if (!force_1sm) {
+    lnmm_bf16_2sm(X, Yt, O, M, K, N, eps, ws, ws_bytes, stream);
+    return;
+  }
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   float* colsum = reinterpret_cast<float*>(wsb);
   int* ready = reinterpret_cast<int*>(wsb + align_up(static_cast<size_t>(N) * 4, 256));

@@ -1,0 +1,367 @@
+// K2 Flash-LayerNorm + MatMul, CTA-pair (cta_group::2) variant.
+//
+// Block program and algebra as in ln_matmul.cu: O = (X Yt^T + mu_neg (x) t4) * rstd
+// with the contraction on RAW X (rules R4/R5). A cluster of two CTAs computes
+// 256x256 output tiles with M=256 tcgen05 MMAs issued by the leader; each CTA
+// stages its own 128 rows of X and half (128 rows) of the Yt tile.
+//
+// Statistics, each computed once and shared through the workspace:
+//   t4 = colsum(Yt): a 1/grid slice per CTA in the epilogue-warp prologue,
+//        published with a grid-wide counter (as in the 1-SM kernel);
+//   t1, t2 (row sums of X and X^2) -> mu_neg, rstd: row tile rt (128 rows) is
+//        reduced from global memory by CTA rt % gridDim in its tile iteration
+//        rt / gridDim (before that iteration's epilogue waits), and published
+//        with a per-row-tile release flag. A tile at cluster iteration i only
+//        needs row tiles < 2 * 74 * (i + 1), all computed at iterations <= i, so
+//        every wait is on work that never waits itself.
+// The SMEM operand stages are read only by the tensor cores.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.hpp"
+#include "sm100.cuh"
+#include "tma_host.hpp"
+
+namespace bfgpu {
+namespace lnmm2 {
+
+constexpr int BM = 128;  // rows per CTA (256 per pair)
+constexpr int BK = 64;
+constexpr int BN = 256;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = 128 * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int OUT_BYTES = BM * 128 * 2;
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_THREADS = 128;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t IDESC = dev::idesc_bf16_f32(256, 256);
+constexpr int NUM_BARS = 2 * STAGES + 2 * 2;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OUT_BYTES + NUM_BARS * 8 + 16;
+
+struct Params {
+  int M, K, N;
+  int Mt, Nt, kt;  // Mt in 256-row units
+  int num_tiles;
+  int group;
+  float inv_k;
+  float eps;
+  const __nv_bfloat16* X;
+  const __nv_bfloat16* Yt;
+  float* colsum;    // [N]
+  float* row_mu;    // [M] -mean
+  float* row_rstd;  // [M]
+  int* col_ready;   // CTAs that published their colsum slice
+  int* row_ready;   // [2*Mt] per 128-row tile: 1 once its statistics are published
+};
+
+__device__ __forceinline__ void decode(const Params& p, int t, int& m, int& n) {
+  // Within a group of m-units, n is the slow index: every (m, 0) tile precedes (m, n>0).
+  const int per_group = p.group * p.Nt;
+  const int g = t / per_group;
+  const int r = t % per_group;
+  const int gs = min(p.group, p.Mt - g * p.group);
+  m = g * p.group + r % gs;
+  n = r / gs;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    ln_matmul_2sm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_y,
+                         const __grid_constant__ CUtensorMap tm_o, const Params p) {
+  using namespace dev;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  uint8_t* stage_base = smem;
+  uint8_t* out_stage = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_stage + OUT_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_y);
+    tma_prefetch_desc(&tm_o);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPI_THREADS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        int m, n;
+        decode(p, t, m, n);
+        const int mrow = m * 2 * BM + static_cast<int>(rank) * BM;
+        for (int k = 0; k < p.kt; ++k) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = stage_base + stage * STAGE_BYTES;
+          const uint32_t fbar = full0 + stage * 8;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          tma_load_2d_2sm(&tm_x, fbar, sa, k * BK, mrow);
+          tma_load_2d_2sm(&tm_y, fbar, sa + A_BYTES, k * BK, n * BN + static_cast<int>(rank) * 128);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc = 0, aphase = 0;
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int k = 0; k < p.kt; ++k) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(stage_base + stage * STAGE_BYTES);
+            const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_bf16_ss_2sm(d_tmem, sdesc_kmajor_sw128(a_addr + kk * 32), sdesc_kmajor_sw128(b_addr + kk * 32),
+                               IDESC, (k | kk) != 0);
+            umma_commit_2sm_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) umma_commit_2sm_mc(&tfull[acc], 0x3);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp & 3;
+    const uint32_t row = q * 32 + lane;
+    const uint32_t etid = threadIdx.x - 4 * 32;
+    const bool store_leader = etid == 0;
+    const uint32_t out_addr = smem_u32(out_stage);
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+
+    // ---- t4 = colsum(Yt): this CTA's slice, one warp per Yt row
+    {
+      const int per = (p.N + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+      const int n0 = static_cast<int>(blockIdx.x) * per, n1 = min(p.N, n0 + per);
+      for (int n = n0 + static_cast<int>(q); n < n1; n += 4) {
+        const float2 mom = warp_row_moments_bf16(p.Yt + static_cast<size_t>(n) * p.K, p.K, lane);
+        if (lane == 0) p.colsum[n] = mom.x;
+      }
+      named_bar_sync(1, EPI_THREADS);
+      if (store_leader) {
+        __threadfence();
+        red_release_gpu_add(p.col_ready, 1);
+      }
+    }
+    bool col_seen = false;
+    const int num_rt = (p.M + BM - 1) / BM;
+    int next_rt = static_cast<int>(blockIdx.x);
+    int iter = 0;
+    auto compute_row_tile = [&](int rt) {
+      for (int rr = static_cast<int>(q); rr < BM; rr += 4) {
+        const int r = rt * BM + rr;
+        if (r >= p.M) break;
+        const float2 mom = warp_row_moments_bf16(p.X + static_cast<size_t>(r) * p.K, p.K, lane);
+        if (lane == 0) {
+          const float mean = mom.x * p.inv_k;
+          // var = t2/total(K) + (0 - square(t1/total(K)))  [+ eps, 0 in the reference]
+          p.row_mu[r] = -mean;
+          p.row_rstd[r] = 1.0f / sqrtf(mom.y * p.inv_k - mean * mean + p.eps);
+        }
+      }
+      named_bar_sync(1, EPI_THREADS);
+      if (store_leader) {
+        __threadfence();
+        red_release_gpu_add(&p.row_ready[rt], 1);
+      }
+    };
+
+    uint32_t acc = 0, aphase = 0;
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      int m, n;
+      decode(p, t, m, n);
+      const int mtile = m * 2 + static_cast<int>(rank);
+      const int row0 = mtile * BM;
+      // ---- t1, t2: row tiles rt = blockIdx.x + i * gridDim.x, one per tile iteration i (so a
+      // row tile is published long before any tile that needs it is reached; see header).
+      while (next_rt < num_rt && next_rt / static_cast<int>(gridDim.x) <= iter) {
+        compute_row_tile(next_rt);
+        next_rt += static_cast<int>(gridDim.x);
+      }
+      ++iter;
+      if (store_leader) {
+        const uint64_t t0 = globaltimer_ns();
+        while ((!col_seen && ld_acquire_gpu(p.col_ready) < static_cast<int>(gridDim.x)) ||
+               (mtile < num_rt && ld_acquire_gpu(&p.row_ready[mtile]) < 1)) {  // no rows: nothing to wait for
+          __nanosleep(128);
+          if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+        }
+      }
+      col_seen = true;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int grow = row0 + static_cast<int>(row);
+      const uint32_t trow = tmem_base + acc * 256 + ((q * 32) << 16);
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        if (store_leader) bulk_wait_read0();
+        named_bar_sync(1, EPI_THREADS);  // staging free; statistics published (leader waited above)
+        const float mu_neg = grow < p.M ? __ldcg(p.row_mu + grow) : 0.f;
+        const float rstd = grow < p.M ? __ldcg(p.row_rstd + grow) : 0.f;
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(trow + half * 128 + j * 32, v);
+          tmem_wait_ld();
+          const int c0 = n * BN + half * 128 + j * 32;
+          float cs[32];
+          if (c0 + 32 <= p.N) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 f = __ldcg(reinterpret_cast<const float4*>(p.colsum + c0) + i);
+              cs[4 * i] = f.x;
+              cs[4 * i + 1] = f.y;
+              cs[4 * i + 2] = f.z;
+              cs[4 * i + 3] = f.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = c0 + i < p.N ? __ldcg(p.colsum + c0 + i) : 0.f;
+          }
+          uint32_t ov[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float o0 = (__uint_as_float(v[2 * i]) + mu_neg * cs[2 * i]) * rstd;
+            const float o1 = (__uint_as_float(v[2 * i + 1]) + mu_neg * cs[2 * i + 1]) * rstd;
+            ov[i] = pack_bf16x2(o0, o1);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int chunk = j * 4 + c;
+            st_shared_v4(out_addr + (chunk >> 3) * (BM * 128) + sw128_offset(row, chunk & 7), ov[4 * c],
+                         ov[4 * c + 1], ov[4 * c + 2], ov[4 * c + 3]);
+          }
+        }
+        if (half == 1) {
+          tc_fence_before();
+          if (leader)
+            mbar_arrive(&tempty[acc]);
+          else
+            mbar_arrive_remote(tempty0 + acc * 8);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, EPI_THREADS);
+        if (store_leader) {
+          tma_store_2d(&tm_o, out_stage, n * BN + half * 128, row0);
+          tma_store_2d(&tm_o, out_stage + BM * 128, n * BN + half * 128 + 64, row0);
+          bulk_commit();
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+    while (next_rt < num_rt) {  // row tiles beyond this CTA's tile count (tiny problems)
+      compute_row_tile(next_rt);
+      next_rt += static_cast<int>(gridDim.x);
+    }
+    if (store_leader) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace lnmm2
+
+extern void note_launch();
+
+size_t lnmm2_workspace_bytes(int64_t M, int64_t N) {
+  const size_t mt = static_cast<size_t>((M + 255) / 256) * 2;
+  return align_up(static_cast<size_t>(N) * 4, 256) + 2 * align_up(static_cast<size_t>(M) * 4, 256) +
+         align_up((mt + 1) * 4, 256);
+}
+
+void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
+                   size_t ws_bytes, cudaStream_t stream) {
+  using namespace lnmm2;
+  BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm2_workspace_bytes(M, N), "bf_layernorm_matmul: workspace too small");
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  Params p{};
+  p.M = static_cast<int>(M);
+  p.K = static_cast<int>(K);
+  p.N = static_cast<int>(N);
+  p.Mt = static_cast<int>((M + 255) / 256);
+  p.Nt = static_cast<int>((N + BN - 1) / BN);
+  p.kt = static_cast<int>((K + BK - 1) / BK);
+  p.group = 8;
+  p.inv_k = 1.0f / static_cast<float>(K);
+  p.eps = eps;
+  p.X = static_cast<const __nv_bfloat16*>(X);
+  p.Yt = static_cast<const __nv_bfloat16*>(Yt);
+  p.colsum = reinterpret_cast<float*>(w);
+  w += align_up(static_cast<size_t>(N) * 4, 256);
+  p.row_mu = reinterpret_cast<float*>(w);
+  w += align_up(static_cast<size_t>(M) * 4, 256);
+  p.row_rstd = reinterpret_cast<float*>(w);
+  w += align_up(static_cast<size_t>(M) * 4, 256);
+  p.col_ready = reinterpret_cast<int*>(w);
+  p.row_ready = p.col_ready + 1;
+  const long long tiles = static_cast<long long>(p.Mt) * p.Nt;
+  BF_CHECK_ARG(tiles < (1ll << 31), "bf_layernorm_matmul: too many tiles");
+  p.num_tiles = static_cast<int>(tiles);
+
+  const CUtensorMap tm_x = make_tmap_bf16(X, M, K, K, BK, BM);
+  const CUtensorMap tm_y = make_tmap_bf16(Yt, N, K, K, BK, 128);
+  const CUtensorMap tm_o = make_tmap_bf16(O, M, N, N, BK, BM);
+  static bool attr_set = false;
+  if (!attr_set) {
+    BF_CUDA(cudaFuncSetAttribute(ln_matmul_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  const int sms = num_sms(current_device());
+  const int clusters = static_cast<int>(std::min<long long>(tiles, sms / 2));
+  BF_CUDA(cudaMemsetAsync(p.col_ready, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
+  ln_matmul_2sm_kernel<<<clusters * 2, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_y, tm_o, p);
+  BF_CUDA(cudaGetLastError());
+  note_launch();
+}
+
+}  // namespace bfgpu

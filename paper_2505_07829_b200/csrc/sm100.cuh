@@ -353,6 +353,44 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar, uint16_t cta_m
       : "memory");
 }
 
+// ------------------------------------------------------------ row reductions ---
+
+// One warp reduces a contiguous bf16 row of length n (multiple of 8): returns
+// (sum x, sum x^2) in every lane. Eight independent 16-byte loads per lane are in
+// flight per step so the loop is bandwidth-, not latency-bound.
+__device__ __forceinline__ float2 warp_row_moments_bf16(const __nv_bfloat16* row, int n, uint32_t lane) {
+  const uint4* p = reinterpret_cast<const uint4*>(row);
+  const int nv = n >> 3;
+  float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+  for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + static_cast<int>(lane);
+      v[u] = c < nv ? __ldg(p + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
+        s1a += lo;
+        s1b += hi;
+        s2a = fmaf(lo, lo, s2a);
+        s2b = fmaf(hi, hi, s2b);
+      }
+    }
+  }
+  float s1 = s1a + s1b, s2 = s2a + s2b;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  return make_float2(s1, s2);
+}
+
 // ------------------------------------------------------------ descriptors ---
 
 // UMMA shared-memory descriptor for a K-major operand staged by TMA with
