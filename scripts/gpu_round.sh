@@ -7,6 +7,9 @@ timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpu
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 2 -c 1 -o gpurun_out/prof_ffn -f python scripts/ncu_target.py ffn_8b fused 3 > gpurun_out/ncu_ffn.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 4 -c 2 -o gpurun_out/prof_ffn2p -f python scripts/ncu_target.py ffn_8b two_phase 3 > gpurun_out/ncu_ffn2p.log 2>&1
-timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+true
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
 lscpu > gpurun_out/lscpu.txt; free -g >> gpurun_out/lscpu.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_matmul -s 2 -c 1 -o gpurun_out/prof_lnmm -f python scripts/ncu_target.py lnmm fused 3 > gpurun_out/ncu_lnmm.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 2 -c 1 -o gpurun_out/prof_attn -f python scripts/ncu_target.py attn fused 3 > gpurun_out/ncu_attn.log 2>&1
+for w in lnmm attn ffn_70b; do timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
