@@ -135,7 +135,17 @@ def ncu_traffic(kernel_key: str):
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        if kernel_key in d:
+            return d[kernel_key].get("dram_bytes_per_launch")
+        # kernel names carry template/variant suffixes (ffn_swiglu_2sm_kernel, attn_kernel<128, 128>):
+        # match on the capture name and the kernel's stem.
+        stem, _, capture = kernel_key.partition("@")
+        stem = stem.replace("_kernel", "")
+        for k, v in d.items():
+            name, _, cap = k.partition("@")
+            if cap == capture and stem in name:
+                return v.get("dram_bytes_per_launch")
+        return None
     except Exception:
         return None
 

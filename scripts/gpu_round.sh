@@ -1,15 +1,17 @@
 #!/bin/bash
-# One GPU session: smoke, bench line, launch list, full ncu capture of the top kernel.
+# One GPU session: tests, smoke, bench lines, launch list, ncu captures of the kernels.
 set -x
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+for w in attn lnmm ffn_70b; do timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 2 -c 1 -o gpurun_out/prof_ffn -f python scripts/ncu_target.py ffn_8b fused 3 > gpurun_out/ncu_ffn.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 4 -c 2 -o gpurun_out/prof_ffn2p -f python scripts/ncu_target.py ffn_8b two_phase 3 > gpurun_out/ncu_ffn2p.log 2>&1
-true
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
-lscpu > gpurun_out/lscpu.txt; free -g >> gpurun_out/lscpu.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_matmul -s 2 -c 1 -o gpurun_out/prof_lnmm -f python scripts/ncu_target.py lnmm fused 3 > gpurun_out/ncu_lnmm.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_attn.csv python bench.py --workload attn --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_attn_under_ncu.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 2 -c 1 -o gpurun_out/prof_attn -f python scripts/ncu_target.py attn fused 3 > gpurun_out/ncu_attn.log 2>&1
-for w in lnmm attn ffn_70b; do timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
+if [ "$FULL" = 1 ]; then
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 2 -c 1 -o gpurun_out/prof_ffn -f python scripts/ncu_target.py ffn_8b fused 3 > gpurun_out/ncu_ffn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_matmul -s 2 -c 1 -o gpurun_out/prof_lnmm -f python scripts/ncu_target.py lnmm fused 3 > gpurun_out/ncu_lnmm.log 2>&1
+fi
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
+true
