@@ -128,6 +128,17 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def unfused_measured(kind: str):
+    """DRAM bytes of one step of the unfused operator sequence (torch/cuBLAS kernels, one per
+    top-level operator), measured with ncu by scripts/unfused_baseline.py (or None)."""
+    p = ROOT / "profiles" / "unfused_baseline.json"
+    key = {"ffn": "ffn_8b", "lnmm": "lnmm", "attn": "attn"}[kind]
+    try:
+        return json.loads(p.read_text()).get(key)
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernel_key: str):
     """dram bytes per launch of the dominant kernel from the committed ncu summary (or None)."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -456,6 +467,8 @@ def run_ours(args, wl):
                 "fused_algorithmic_per_gpu": inp["fused_bytes"], "unfused_op_sequence_per_gpu": inp["unfused_bytes"],
                 "unfused_over_fused": inp["unfused_bytes"] / inp["fused_bytes"], "reference_model": model,
                 "measured_ncu_per_launch": ncu_traffic(f"{kkey}@{capture}"),
+                "measured_unfused_ncu_per_step": (unfused_measured(kind) or {}).get("dram_bytes_per_step")
+                if wl["name"].startswith(("C3", "C4", "C2")) else None,
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -8,16 +8,19 @@
 // Statistics, each computed once and shared through the workspace:
 //   t4 = colsum(Yt): a 1/grid slice per CTA in the epilogue-warp prologue,
 //        published with a grid-wide counter (as in the 1-SM kernel);
-//   t1, t2 (row sums of X and X^2) -> mu_neg, rstd: row tile rt (128 rows) is
-//        reduced from global memory by CTA rt % gridDim in its tile iteration
-//        rt / gridDim (before that iteration's epilogue waits), and published
-//        with a per-row-tile release flag. A tile at cluster iteration i only
-//        needs row tiles < 2 * 74 * (i + 1), all computed at iterations <= i, so
-//        every wait is on work that never waits itself.
+//   t1, t2 (row sums of X and X^2) -> mu_neg, rstd: the 128 rows of a CTA's half
+//        of m-unit m are reduced from global memory by the CTA whose tile (m, 0)
+//        (the m-unit's first n-tile) comes next: it does so after its current
+//        epilogue, one mainloop before the tile (m, 0) streams the same rows, so
+//        they are still in L2 and X is read from HBM once. The statistics are
+//        published with a per-row-tile release flag. Computing statistics never
+//        waits, and (m, 0) precedes every (m, n) in the tile order, so every wait
+//        is on work that never waits itself.
 // The SMEM operand stages are read only by the tensor cores.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "sm100.cuh"
@@ -188,8 +191,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     bool col_seen = false;
     const int num_rt = (p.M + BM - 1) / BM;
-    int next_rt = static_cast<int>(blockIdx.x);
-    int iter = 0;
     auto compute_row_tile = [&](int rt) {
       for (int rr = static_cast<int>(q); rr < BM; rr += 4) {
         const int r = rt * BM + rr;
@@ -215,13 +216,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       decode(p, t, m, n);
       const int mtile = m * 2 + static_cast<int>(rank);
       const int row0 = mtile * BM;
-      // ---- t1, t2: row tiles rt = blockIdx.x + i * gridDim.x, one per tile iteration i (so a
-      // row tile is published long before any tile that needs it is reached; see header).
-      while (next_rt < num_rt && next_rt / static_cast<int>(gridDim.x) <= iter) {
-        compute_row_tile(next_rt);
-        next_rt += static_cast<int>(gridDim.x);
-      }
-      ++iter;
+      // ---- t1, t2 of this CTA's rows are produced by the CTA that owns the m-unit's
+      // first n-tile (see header); in the first wave nobody ran ahead, so do it now.
+      if (t == cluster_id && n == 0 && mtile < num_rt) compute_row_tile(mtile);
       if (store_leader) {
         const uint64_t t0 = globaltimer_ns();
         while ((!col_seen && ld_acquire_gpu(p.col_ready) < static_cast<int>(gridDim.x)) ||
@@ -290,12 +287,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           bulk_commit();
         }
       }
+      // Statistics for the next tile's rows if it opens an m-unit: they are read here,
+      // one mainloop ahead of that tile's X stream, which then finds the rows in L2
+      // (X leaves HBM once), and ahead of every other tile of the m-unit.
+      const int tn = t + num_clusters;
+      if (tn < p.num_tiles) {
+        int m2, n2;
+        decode(p, tn, m2, n2);
+        const int mt2 = m2 * 2 + static_cast<int>(rank);
+        if (n2 == 0 && mt2 < num_rt) compute_row_tile(mt2);
+      }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
-    }
-    while (next_rt < num_rt) {  // row tiles beyond this CTA's tile count (tiny problems)
-      compute_row_tile(next_rt);
-      next_rt += static_cast<int>(gridDim.x);
     }
     if (store_leader) bulk_wait0();
   }
@@ -331,7 +334,15 @@ void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K,
   p.Mt = static_cast<int>((M + 255) / 256);
   p.Nt = static_cast<int>((N + BN - 1) / BN);
   p.kt = static_cast<int>((K + BK - 1) / BK);
-  p.group = 8;
+  // m-units (256 rows) per scheduling group; n is the slow index inside a group, so the
+  // group's X rows (16 x 2 MB at K = 4096) stay in L2 while its n-tiles pass. Measured at
+  // C4 (scripts/exp_lnmm.sh): g = 2/4/8/16/32 -> 993/1382/1398/1481/1386 TFLOP/s, DRAM
+  // 1.39/1.41/1.88/1.89/3.23 GB per launch.
+  static const int group_env = [] {
+    const char* v = std::getenv("BFGPU_LNMM_GROUP");
+    return v ? std::atoi(v) : 0;
+  }();
+  p.group = group_env > 0 ? group_env : 16;
   p.inv_k = 1.0f / static_cast<float>(K);
   p.eps = eps;
   p.X = static_cast<const __nv_bfloat16*>(X);

@@ -1,4 +1,6 @@
-timeout 300 python -m pytest tests/test_lnmm_gpu.py tests/test_ffn_gpu.py -q --tb=line -x 2>&1 | tail -3
-timeout 100 python scripts/debug_bitwise.py 2>&1
-echo "2SM:"; timeout 120 python scripts/quick_perf.py lnmm ffn 2>&1
-echo "1SM:"; BFGPU_LNMM_1SM=1 timeout 120 python scripts/quick_perf.py lnmm 2>&1 | head -1
+#!/bin/bash
+mkdir -p gpurun_out
+for g in 2 4 8 16 32; do echo "group=$g"
+BFGPU_LNMM_GROUP=$g timeout 120 python scripts/quick_perf.py lnmm 2>&1 | grep 'K2:'
+BFGPU_LNMM_GROUP=$g timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:ln_matmul -s 2 -c 1 --csv python scripts/ncu_target.py lnmm fused 3 2>/dev/null | grep -E 'dram__bytes' | awk -F'","' '{print $(NF-2), $(NF-1), $NF}'
+done
