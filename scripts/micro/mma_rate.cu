@@ -8,7 +8,8 @@ using namespace bfgpu::dev;
 
 __device__ int g_mode_st = 0;
 __global__ void set_mode(int v) { g_mode_st = v; }
-// MODE 0: SS N=128, 1: SS N=256, 2: TS N=128, 3: attention group sequence (TS x8, commit, SS x8, commit)
+// MODE 0: SS N=128, 1: SS N=256, 2: TS N=128, 3: attention group sequence (TS x8, commit, SS x8, commit),
+//      4: SS N=64, 5: TS N=64
 template <int MODE>
 __global__ void __launch_bounds__(384, 1) mma_bench(int iters, int ldwarps, unsigned long long* out, uint32_t* sink) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -22,7 +23,7 @@ __global__ void __launch_bounds__(384, 1) mma_bench(int iters, int ldwarps, unsi
   if (warp == 0) tmem_alloc<512>(&slot);
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = slot;
-  constexpr uint32_t N = MODE == 1 ? 256 : 128;
+  constexpr uint32_t N = MODE == 1 ? 256 : (MODE >= 4 ? 64 : 128);
   constexpr uint32_t idesc = idesc_bf16_f32(128, N);
   unsigned long long t0 = clock64();
   if (warp == 8) {
@@ -34,6 +35,8 @@ __global__ void __launch_bounds__(384, 1) mma_bench(int iters, int ldwarps, unsi
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           if (MODE == 3) {
             umma_bf16_ts(tmem + 256 + (it & 1) * 128, tmem + (it & 1) * 128 + kk * 8, sdesc_kmajor_sw128(b + off), idesc, 1);
+          } else if (MODE == 5) {
+            umma_bf16_ts(tmem + 256, tmem + 128 + kk * 8, sdesc_kmajor_sw128(b + off), idesc, 1);
           } else if (MODE == 2)
             umma_bf16_ts(tmem + 256, tmem + 128 + kk * 8, sdesc_kmajor_sw128(b + off), idesc, 1);
           else
@@ -113,7 +116,7 @@ void run(const char* name, int ldw, unsigned long long* d_out, uint32_t* sink) {
   cudaDeviceSynchronize();
   unsigned long long h;
   cudaMemcpy(&h, d_out, 8, cudaMemcpyDeviceToHost);
-  const double N = MODE == 1 ? 256 : 128;
+  const double N = MODE == 1 ? 256 : (MODE >= 4 ? 64 : 128);
   const double cyc_per_instr = double(h) / (iters * (MODE == 3 ? 16.0 : 8.0));
   printf("%-18s ldwarps=%d  cycles/MMA(K=16)=%.1f  ideal=%.0f  eff=%.0f%%   err=%s\n", name, ldw, cyc_per_instr, N / 2,
          100.0 * (N / 2) / cyc_per_instr, cudaGetErrorString(cudaGetLastError()));
@@ -122,11 +125,13 @@ void run(const char* name, int ldw, unsigned long long* d_out, uint32_t* sink) {
 int main() {
   unsigned long long* d_out; uint32_t* sink;
   cudaMalloc(&d_out, 8 * 148); cudaMalloc(&sink, 4 * 384 * 148);
-  for (int st : {4}) set_mode<<<1, 1>>>(st), cudaDeviceSynchronize(), printf("side load: %s\n", st == 0 ? "tcgen05.ld" : st == 2 ? "mbarrier try_wait spinners" : st == 3 ? "st.shared stream" : "MUFU+FFMA2 stream"),
+  for (int st : {0}) set_mode<<<1, 1>>>(st), cudaDeviceSynchronize(), printf("side load: %s\n", st == 0 ? "tcgen05.ld" : st == 2 ? "mbarrier try_wait spinners" : st == 3 ? "st.shared stream" : "MUFU+FFMA2 stream"),
   [&] { for (int ldw : {0, 8}) {
     run<0>("SS 128x128", ldw, d_out, sink);
     run<1>("SS 128x256", ldw, d_out, sink);
     run<2>("TS 128x128", ldw, d_out, sink);
     run<3>("TSx8+SSx8 groups", ldw, d_out, sink);
+    run<4>("SS 128x64", ldw, d_out, sink);
+    run<5>("TS 128x64", ldw, d_out, sink);
   } }();
 }
