@@ -400,11 +400,11 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
     const char* v = std::getenv("BFGPU_FFN_GROUP");
     return v ? std::atoi(v) : 0;
   }();
-  // Default: about 120 MB of H per group (32 m-tiles at ffn=14336, 16 at ffn=28672),
-  // measured best at the Llama-3-8B shape (g=8: 1226, g=16: 1304, g=32: 1417, g=64: 1251 TFLOP/s).
-  int g = static_cast<int>((120ll << 20) / (static_cast<long long>(BM) * F * 2));
-  int g2 = 4;
-  while (g2 * 2 <= g && g2 < 64) g2 *= 2;
+  // Default: 32 m-tiles (4096 rows) per group. Measured (TFLOP/s, fused, 2-SM):
+  //   Llama-3-8B  (C3): g=16 1470, g=32 1581, g=64 1477 (1-SM: 1226 / 1304 / 1417 / 1251 at 8/16/32/64)
+  //   Llama-3-70B (C5, power-capped): g=16 941-964, g=32 1016, g=64 1000-1024, g=128 983
+  // Smaller groups re-read the weights more often; larger ones let H and X thrash L2.
+  const int g2 = 32;
   p.group = group_env > 0 ? group_env : std::min(g2, p.Mt);
 
   // CTA-pair path (default): 256-row m-units, B split across the pair.
