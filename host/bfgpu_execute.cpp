@@ -207,6 +207,13 @@ Precision env_precision() {
   return Precision::BF16;
 }
 
+Route env_route() {
+  const char* v = std::getenv("BFGPU_ROUTE");
+  if (v && std::strcmp(v, "fused") == 0) return Route::Fused;
+  if (v && std::strcmp(v, "generic") == 0) return Route::Generic;
+  return Route::Auto;
+}
+
 }  // namespace
 
 Recognized recognize(const BlockGraph& program) {
@@ -237,7 +244,20 @@ Recognized recognize(const BlockGraph& program) {
 
 std::map<std::string, Matrix> execute(const BlockGraph& program, const std::map<std::string, Matrix>& inputs,
                                       const DimBinding& binding, const ExecConfig& cfg) {
-  const Recognized rec = recognize(program);
+  return execute_routed(program, inputs, binding, cfg, blockfuse::ExecOptions{});
+}
+
+std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const std::map<std::string, Matrix>& inputs,
+                                             const DimBinding& binding, const ExecConfig& cfg,
+                                             const blockfuse::ExecOptions& opts) {
+  if (cfg.route == Route::Generic) return execute_generic(program, inputs, binding, opts, cfg.stream);
+  Recognized rec;
+  try {
+    rec = recognize(program);
+  } catch (const Error&) {
+    if (cfg.route == Route::Fused) throw;
+    return execute_generic(program, inputs, binding, opts, cfg.stream);
+  }
   const int dt = cfg.precision == Precision::BF16 ? BF_DTYPE_BF16 : BF_DTYPE_F32;
   const size_t eb = cfg.precision == Precision::BF16 ? 2 : 4;
   void* s = cfg.stream;
@@ -295,10 +315,10 @@ std::map<std::string, Matrix> execute(const BlockGraph& program, const std::map<
 
 std::map<std::string, Matrix> execute(const BlockGraph& program, const std::map<std::string, Matrix>& inputs,
                                       const DimBinding& binding, const blockfuse::ExecOptions& opts) {
-  (void)opts;  // fused candidates contain no Misc nodes, so the misc registry is never consulted
   ExecConfig cfg;
   cfg.precision = env_precision();
-  return execute(program, inputs, binding, cfg);
+  cfg.route = env_route();
+  return execute_routed(program, inputs, binding, cfg, opts);  // opts.misc serves the generic route's Misc nodes
 }
 
 }  // namespace bfgpu

@@ -7,8 +7,9 @@
 // graph on the CPU in float64, it recognizes the fused candidate the fusion
 // driver emitted (every snapshot of fuse(lower(examples::X())), engine.hpp:164)
 // and runs it as one hand-written sm_100a kernel through the C-ABI in
-// include/bfgpu.h. Unrecognized programs are an error (blockfuse::Error): there
-// is no CPU fallback.
+// include/bfgpu.h. Any other program (unfused lower() output, partial fusions,
+// programs with Misc nodes) runs on the generic float64 GPU route. There is no
+// CPU fallback: every operator runs on the device.
 //
 // Build: against the reference headers (proj/include) and the same
 // <Eigen/Dense> the reference build uses; links libbfgpu.so.
@@ -26,9 +27,17 @@ enum class Precision {
   F32,   // fp32 in / fp32 out on the FMA pipes (matches float64 within 1e-4)
 };
 
+// Which executor runs a program.
+enum class Route {
+  Auto,     // the fused sm_100a kernel if the program is a recognized fused candidate, else Generic
+  Fused,    // recognized fused candidates only; anything else throws blockfuse::Error
+  Generic,  // the generic float64 GPU walk (bfgpu_generic.cpp) for any program
+};
+
 struct ExecConfig {
-  Precision precision = Precision::BF16;
-  void* stream = nullptr;  // cudaStream_t; nullptr = legacy default stream
+  Precision precision = Precision::BF16;  // fused kernels only; the generic route is float64
+  void* stream = nullptr;                 // cudaStream_t; nullptr = legacy default stream
+  Route route = Route::Auto;
 };
 
 enum class Pattern { RmsFfnSwiglu, LayerNormMatMul, Attention };
@@ -46,7 +55,17 @@ struct Recognized {
 // Throws blockfuse::Error for anything else.
 Recognized recognize(const blockfuse::BlockGraph& program);
 
-// Precision from BFGPU_PRECISION (bf16 | f32), default bf16.
+// Any block program on the GPU in float64: the reference's eval_graph/eval_map walk
+// (interpreter.hpp:301-472) with device-resident values and one generic kernel per
+// operator (csrc/generic.cu). Misc nodes call the executors in `opts` on host values.
+std::map<std::string, blockfuse::Matrix> execute_generic(const blockfuse::BlockGraph& program,
+                                                         const std::map<std::string, blockfuse::Matrix>& inputs,
+                                                         const blockfuse::DimBinding& binding,
+                                                         const blockfuse::ExecOptions& opts = {},
+                                                         void* stream = nullptr);
+
+// Precision from BFGPU_PRECISION (bf16 | f32), default bf16; route from BFGPU_ROUTE
+// (auto | fused | generic), default auto.
 std::map<std::string, blockfuse::Matrix> execute(const blockfuse::BlockGraph& program,
                                                  const std::map<std::string, blockfuse::Matrix>& inputs,
                                                  const blockfuse::DimBinding& binding,
@@ -55,5 +74,11 @@ std::map<std::string, blockfuse::Matrix> execute(const blockfuse::BlockGraph& pr
 std::map<std::string, blockfuse::Matrix> execute(const blockfuse::BlockGraph& program,
                                                  const std::map<std::string, blockfuse::Matrix>& inputs,
                                                  const blockfuse::DimBinding& binding, const ExecConfig& cfg);
+
+// Both of the above: route per cfg.route, Misc executors from opts (generic route).
+std::map<std::string, blockfuse::Matrix> execute_routed(const blockfuse::BlockGraph& program,
+                                                        const std::map<std::string, blockfuse::Matrix>& inputs,
+                                                        const blockfuse::DimBinding& binding, const ExecConfig& cfg,
+                                                        const blockfuse::ExecOptions& opts);
 
 }  // namespace bfgpu

@@ -48,6 +48,14 @@ _SIGNATURES = [
         ctypes.c_int,
         [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, _vp],
     ),
+    ("bf_gx_binary", ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, _i64, _vp]),
+    ("bf_gx_row_op", ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _vp]),
+    ("bf_gx_row_sum", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp]),
+    ("bf_gx_dot", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    ("bf_gx_outer", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    ("bf_gx_elementwise", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp]),
+    ("bf_gx_copy2d", ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    ("bf_gx_zero", ctypes.c_int, [_vp, _i64, _vp]),
     ("bf_device_alloc", ctypes.c_void_p, [ctypes.c_size_t]),
     ("bf_device_free", ctypes.c_int, [_vp]),
     ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),

@@ -98,6 +98,35 @@ def test_verify_every_snapshot_against_reference_interpreter(example, dims, bloc
         assert "verdict: equivalent" in r.stdout
 
 
+# the generic float64 GPU route (host/bfgpu_generic.cpp) on programs no fused kernel covers
+GENERIC = [
+    ("attention", "M=2,N=2,D=2,L=2", "4x4", ""),
+    ("layernorm-matmul", "M=2,N=2,K=2", "4x4", ""),
+    ("rms-swiglu", "M=2,N=2,K=2,D=2", "4x4", ""),
+    ("rms-swiglu", "M=3,N=2,K=4,D=1", "4x4", "M=2,N=3,K=2,D=4"),  # asymmetric, test_engine.cpp:221-238
+    ("attention", "M=3,N=2,D=1,L=2", "4x4", "M=2,N=3,D=4,L=2"),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("example,dims,block,lens", GENERIC)
+def test_generic_route_runs_unfused_and_every_snapshot(example, dims, block, lens):
+    _, count = EXAMPLES[example]
+    files = ["lowered.json"] + [f"snapshot_{k}.json" for k in range(1, count + 1)]
+    for f in files:
+        args = ["verify", PROGRAMS / example / f, "--dims", dims, "--block", block, "--trials", 2, "--route", "generic"]
+        if lens:
+            args += ["--len", lens]
+        r = cli(*args, check=0)
+        assert "route: generic f64" in r.stdout and "verdict: equivalent" in r.stdout, f
+    # auto routes the unfused program to the generic executor, the fused ones to their kernels
+    r = cli("verify", PROGRAMS / example / "lowered.json", "--dims", dims, "--block", block, "--trials", 1,
+            *(["--len", lens] if lens else []), check=0)
+    assert "route: generic f64" in r.stdout
+    r = cli("verify", PROGRAMS / example / "lowered.json", "--dims", dims, "--block", block, "--route", "fused", check=1)
+    assert "no CPU fallback" in r.stderr
+
+
 @pytest.mark.gpu
 def test_run_reports_output():
     r = cli("run", PROGRAMS / "rms-swiglu" / "snapshot_3.json", "--dims", "M=2,N=2,K=3,D=2", "--block", "128x128",

@@ -13,6 +13,9 @@
 //                        [--seed 42] [--precision bf16|f32] [--repeat R]
 //   bfgpu-cli verify     <program.json> --dims ... [--block] [--len] [--trials 3]
 //                        [--seed 42] [--tol T] [--precision bf16|f32]
+// run/verify take --route auto|fused|generic: auto runs recognized fused candidates on
+// their sm_100a kernel and anything else (e.g. an unfused lowered.json) on the generic
+// float64 GPU route (host/bfgpu_generic.cpp).
 //
 // `snapshots` is the reference's own fuse(lower(examples::X())) (engine.hpp:164) written
 // with its serializer; it exists because the reference CLI needs CLI11, absent here.
@@ -110,6 +113,15 @@ DimBinding parse_binding(const Args& a) {
 
 bfgpu::ExecConfig exec_config(const Args& a) {
   bfgpu::ExecConfig cfg;
+  const std::string route = a.get("route", "auto");
+  if (route == "auto")
+    cfg.route = bfgpu::Route::Auto;
+  else if (route == "fused")
+    cfg.route = bfgpu::Route::Fused;
+  else if (route == "generic")
+    cfg.route = bfgpu::Route::Generic;
+  else
+    throw Error("--route must be auto, fused or generic");
   const std::string prec = a.get("precision", "bf16");
   if (prec == "bf16")
     cfg.precision = bfgpu::Precision::BF16;
@@ -202,8 +214,18 @@ int cmd_verify(const Args& a) {
   const BlockGraph g = load_block(a.pos[0]);
   const DimBinding b = parse_binding(a);
   const bfgpu::ExecConfig cfg = exec_config(a);
-  const bool bf16 = cfg.precision == bfgpu::Precision::BF16;
-  const double tol = std::stod(a.get("tol", bf16 ? "2e-2" : "1e-4"));
+  // which executor will run it: a fused kernel (bf16 or fp32) or the generic float64 route
+  bool fused = cfg.route != bfgpu::Route::Generic;
+  if (fused) {
+    try {
+      bfgpu::recognize(g);
+    } catch (const Error&) {
+      if (cfg.route == bfgpu::Route::Fused) throw;
+      fused = false;
+    }
+  }
+  const bool bf16 = fused && cfg.precision == bfgpu::Precision::BF16;
+  const double tol = std::stod(a.get("tol", !fused ? "1e-10" : (bf16 ? "2e-2" : "1e-4")));
   const int trials = std::stoi(a.get("trials", "3"));
   const unsigned long long seed = std::stoull(a.get("seed", "42"));
   const auto specs = input_specs(g, b);
@@ -238,7 +260,8 @@ int cmd_verify(const Args& a) {
     }
   }
   const bool pass = worst <= tol;
-  std::cout << "trials: " << trials << "\n"
+  std::cout << "route: " << (fused ? (bf16 ? "fused bf16" : "fused f32") : "generic f64") << "\n"
+            << "trials: " << trials << "\n"
             << "max |gpu - reference| / max |reference|: " << worst << " (tolerance " << tol << ")\n"
             << "verdict: " << (pass ? "equivalent" : "NOT equivalent") << "\n";
   return pass ? 0 : 2;
