@@ -438,6 +438,8 @@ def run_ours(args, wl):
         kkey = {"ffn": "ffn_swiglu_kernel", "lnmm": "ln_matmul_kernel", "attn": "attn_kernel"}[kind]
         capture = {"ffn": "prof_ffn" if args.schedule == "fused" else "prof_ffn2p", "lnmm": "prof_lnmm",
                    "attn": "prof_attn"}[kind]
+        if wl["name"].startswith("C5"):
+            capture = "prof_ffn70b"  # the C3 capture does not describe the 70B shape
         line = {
             "metric": METRIC,
             "value": value,
