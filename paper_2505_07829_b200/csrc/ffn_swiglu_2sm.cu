@@ -198,9 +198,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (p.mode != kDownOnly) {
       const int per = (p.M + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
       const int r0 = static_cast<int>(blockIdx.x) * per, r1 = min(p.M, r0 + per);
-      for (int r = r0 + static_cast<int>(q); r < r1; r += 4) {
-        const float2 mom = warp_row_moments_bf16(ex.X + static_cast<size_t>(r) * p.D, p.D, lane);
-        if (lane == 0) ex.rstat[r] = 1.0f / sqrtf(mom.y * p.inv_d + p.eps);
+      // four rows per warp at a time (32 loads per lane in flight): the first epilogue waits
+      // for every CTA's slice, so this prologue is on the critical path
+      for (int r = r0 + 4 * static_cast<int>(q); r < r1; r += 16) {
+        const __nv_bfloat16* rows[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rows[k] = ex.X + static_cast<size_t>(min(r + k, r1 - 1)) * p.D;
+        float t1[4], t2[4];
+        warp_rows_moments_bf16<4>(rows, p.D, lane, t1, t2);
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (r + k < r1) ex.rstat[r + k] = 1.0f / sqrtf(t2[k] * p.inv_d + p.eps);
       }
       named_bar_sync(1, EPI_THREADS);
       if (store_leader) {

@@ -30,6 +30,9 @@ namespace bfgpu {
 namespace lnmm2 {
 
 constexpr int BM = 128;  // rows per CTA (256 per pair)
+#ifndef LNMM_STAT_ROWS
+#define LNMM_STAT_ROWS 4
+#endif
 constexpr int BK = 64;
 constexpr int BN = 256;
 constexpr int STAGES = 6;
@@ -191,17 +194,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     bool col_seen = false;
     const int num_rt = (p.M + BM - 1) / BM;
+    auto publish = [&](int r, float t1, float t2) {
+      const float mean = t1 * p.inv_k;
+      // var = t2/total(K) + (0 - square(t1/total(K)))  [+ eps, 0 in the reference]
+      p.row_mu[r] = -mean;
+      p.row_rstd[r] = 1.0f / sqrtf(t2 * p.inv_k - mean * mean + p.eps);
+    };
     auto compute_row_tile = [&](int rt) {
-      for (int rr = static_cast<int>(q); rr < BM; rr += 4) {
-        const int r = rt * BM + rr;
-        if (r >= p.M) break;
-        const float2 mom = warp_row_moments_bf16(p.X + static_cast<size_t>(r) * p.K, p.K, lane);
-        if (lane == 0) {
-          const float mean = mom.x * p.inv_k;
-          // var = t2/total(K) + (0 - square(t1/total(K)))  [+ eps, 0 in the reference]
-          p.row_mu[r] = -mean;
-          p.row_rstd[r] = 1.0f / sqrtf(mom.y * p.inv_k - mean * mean + p.eps);
-        }
+      // kRows rows per warp at a time: these loads stream while the tensor cores run, and
+      // the CTA must finish them within about one mainloop (measured at C4, TFLOP/s:
+      // 1 row at a time 1456-1469, 2 rows 1509-1525, 4 rows 1512, 8 rows 1512)
+      constexpr int kRows = LNMM_STAT_ROWS;
+      for (int rr = kRows * static_cast<int>(q); rr < BM; rr += 4 * kRows) {
+        const int r0 = rt * BM + rr;
+        if (r0 >= p.M) break;
+        const __nv_bfloat16* rows[kRows];
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) rows[k] = p.X + static_cast<size_t>(min(r0 + k, p.M - 1)) * p.K;
+        float t1[kRows], t2[kRows];
+        warp_rows_moments_bf16<kRows>(rows, p.K, lane, t1, t2);
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < kRows; ++k)
+            if (r0 + k < p.M) publish(r0 + k, t1[k], t2[k]);
       }
       named_bar_sync(1, EPI_THREADS);
       if (store_leader) {

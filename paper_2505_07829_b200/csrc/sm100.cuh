@@ -458,6 +458,46 @@ __device__ __forceinline__ float2 warp_row_moments_bf16(const __nv_bfloat16* row
   return make_float2(s1, s2);
 }
 
+// R rows at once (8R independent 16-byte loads per lane in flight): sum x into s1[r] and
+// sum x^2 into s2[r] for row rows[r], in every lane. For statistics that must stream from
+// L2/HBM while the tensor cores run: R times the bytes in flight of the one-row version.
+template <int R>
+__device__ __forceinline__ void warp_rows_moments_bf16(const __nv_bfloat16* const (&rows)[R], int n, uint32_t lane,
+                                                       float (&s1)[R], float (&s2)[R]) {
+  const int nv = n >> 3;
+#pragma unroll
+  for (int r = 0; r < R; ++r) s1[r] = s2[r] = 0.f;
+  for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
+    uint4 v[R][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int c = c0 + u * 32 + static_cast<int>(lane);
+        v[r][u] = c < nv ? __ldg(reinterpret_cast<const uint4*>(rows[r]) + c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t w[4] = {v[r][u].x, v[r][u].y, v[r][u].z, v[r][u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
+          s1[r] += lo + hi;
+          s2[r] = fmaf(lo, lo, fmaf(hi, hi, s2[r]));
+        }
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      s1[r] += __shfl_xor_sync(0xffffffffu, s1[r], o);
+      s2[r] += __shfl_xor_sync(0xffffffffu, s2[r], o);
+    }
+}
+
 // ------------------------------------------------------------ descriptors ---
 
 // UMMA shared-memory descriptor for a K-major operand staged by TMA with

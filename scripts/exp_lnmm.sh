@@ -1,6 +1,7 @@
 #!/bin/bash
-mkdir -p gpurun_out
-for g in 2 4 8 16 32; do echo "group=$g"
-BFGPU_LNMM_GROUP=$g timeout 120 python scripts/quick_perf.py lnmm 2>&1 | grep 'K2:'
-BFGPU_LNMM_GROUP=$g timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:ln_matmul -s 2 -c 1 --csv python scripts/ncu_target.py lnmm fused 3 2>/dev/null | grep -E 'dram__bytes' | awk -F'","' '{print $(NF-2), $(NF-1), $NF}'
+cp paper_2505_07829_b200/lib/libbfgpu.so /tmp/libbfgpu_R2.so
+for R in 1 2 4 8; do
+  if [ $R != 2 ]; then cp variants/libbfgpu_R$R.so paper_2505_07829_b200/lib/libbfgpu.so; else cp /tmp/libbfgpu_R2.so paper_2505_07829_b200/lib/libbfgpu.so; fi
+  echo "rows=$R: $(timeout 120 python scripts/quick_perf.py lnmm 2>&1 | grep 'K2:')  $(timeout 120 python scripts/quick_perf.py lnmm 2>&1 | grep 'K2:')"
 done
+cp /tmp/libbfgpu_R2.so paper_2505_07829_b200/lib/libbfgpu.so
