@@ -1,0 +1,63 @@
+"""Parity of the non-default kernel variants that the environment selects (read once per
+process, hence the subprocesses): the 1-SM K1 and K2 kernels (BFGPU_FFN_1SM, BFGPU_LNMM_1SM),
+the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU) and non-default K1 scheduling groups
+(BFGPU_FFN_GROUP). Same oracle and tolerances as the default-path tests."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from helpers import assert_bf16_close, bf16_round
+from oracle import cpu
+from paper_2505_07829_b200 import ops
+rng = np.random.default_rng(7)
+def t(a): return torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
+what = {what!r}
+if what == "ffn":
+    M, D, F, N = 520, 256, 392, 264
+    X = bf16_round(rng.standard_normal((M, D))); Wt = bf16_round(rng.standard_normal((F, D)) / 16)
+    Vt = bf16_round(rng.standard_normal((F, D)) / 16); Ut = bf16_round(rng.standard_normal((N, F)) / 16)
+    for sched in ("fused", "two_phase"):
+        out = ops.rms_ffn_swiglu(t(X), t(Wt), t(Vt), t(Ut), schedule=sched).double().cpu().numpy()
+        assert_bf16_close(out, cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 variant " + sched)
+elif what == "lnmm":
+    M, K, N = 600, 264, 392
+    X = bf16_round(rng.standard_normal((M, K)) * 3 + 1.5); Yt = bf16_round(rng.standard_normal((N, K)))
+    out = ops.layernorm_matmul(t(X), t(Yt)).double().cpu().numpy()
+    assert_bf16_close(out, cpu.layernorm_matmul(X, Yt), "K2 variant")
+else:
+    Q = bf16_round(rng.standard_normal((3, 300, 128))); K = bf16_round(rng.standard_normal((3, 456, 128)))
+    Vt = bf16_round(rng.standard_normal((3, 128, 456)))
+    out = ops.attention(t(Q), t(K), t(Vt)).double().cpu().numpy()
+    assert_bf16_close(out, cpu.attention_safe(Q, K, Vt), "K3 variant", norm_tol=2e-2)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize(
+    "what,env",
+    [
+        ("ffn", {"BFGPU_FFN_1SM": "1"}),
+        ("ffn", {"BFGPU_FFN_GROUP": "1"}),
+        ("ffn", {"BFGPU_FFN_GROUP": "64"}),
+        ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
+        ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
+        ("attn", {"BFGPU_ATTN_EMU": "8"}),
+        ("attn", {"BFGPU_ATTN_EMU": "12"}),
+        ("attn", {"BFGPU_ATTN_EMU": "16"}),
+    ],
+)
+def test_variant_matches_oracle(what, env):
+    code = SNIPPET.format(root=str(ROOT), tests=str(ROOT / "tests"), what=what)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, **env})
+    assert r.returncode == 0 and "ok" in r.stdout, f"{env}\n{r.stdout}\n{r.stderr[-3000:]}"
