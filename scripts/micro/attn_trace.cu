@@ -49,7 +49,7 @@ int main() {
   printf("err=%s  %.3f ms  %.1f TFLOP/s\n", cudaGetErrorString(cudaGetLastError()), ms, 4.0 * BH * S * S * D / ms / 1e9);
   std::vector<unsigned long long> t(4 * 64 * 8);
   cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
-  unsigned long long base = t[(0 * 64 + 16) * 8 + 0];
+  unsigned long long base = t[(0 * 64 + 10) * 8 + 0];
   printf("blk | WG0: wait  S_ready  loaded  exp_done  arrived | WG1: same | MMA tile0: p_seen token pv_h0h1 mmas_issued commits_done | tile1: same\n");
   printf("MMA waits: tile0 p_seen tma_ok (unused) token | tile1 same\n");
   for (int g = 16; g < 22; ++g) {
@@ -57,7 +57,12 @@ int main() {
     printf("%3d | %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld\n", g, v(2, 0), v(2, 5), v(2, 6), v(2, 2), v(3, 0),
            v(3, 5), v(3, 6), v(3, 2));
   }
-  for (int g = 16; g < 26; ++g) {
+  printf("epilogue of the tile ending at block 15 (WG0 | WG1): enter o_full_seen after_half(last)\n");
+  {
+    auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + 15) * 8 + k] - base); };
+    printf("    %6lld %6lld %6lld | %6lld %6lld %6lld\n", v(0, 5), v(0, 6), v(0, 7), v(1, 5), v(1, 6), v(1, 7));
+  }
+  for (int g = 10; g < 22; ++g) {
     auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + g) * 8 + k] - base); };
     printf("%3d | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld\n",
            g, v(0, 0), v(0, 1), v(0, 2), v(0, 3), v(0, 4), v(1, 0), v(1, 1), v(1, 2), v(1, 3), v(1, 4), v(2, 0), v(2, 2),
