@@ -22,6 +22,7 @@
  *     attention is [Dv, Skv].
  *   - All pointers are device pointers owned by the caller; outputs are
  *     fully overwritten. `stream` is a cudaStream_t (NULL = legacy stream).
+ *     BF16 buffers (and workspaces) must be 16-byte aligned (TMA).
  *   - Return BF_OK (0) on success, otherwise a BF_ERR_* code; the message is
  *     available from bf_last_error() on the calling thread. This mirrors the
  *     reference's `blockfuse::Error` exceptions (ir.hpp:20-23).

@@ -35,6 +35,10 @@ int num_sms(int device) {
   return cache[device];
 }
 
+// TMA tensor maps and the 16-byte vector loads need 16-byte aligned bases (the row
+// strides are checked per kernel as multiples of 8 elements).
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 static void require_sm100() {
   const int dev = current_device();
   int major = 0, minor = 0;
@@ -94,6 +98,9 @@ int bf_rms_ffn_swiglu(const void* X, const void* Wt, const void* Vt, const void*
                       size_t workspace_bytes, void* stream) {
   return guarded([&] {
     BF_CHECK_ARG(X && Wt && Vt && Ut && O, "bf_rms_ffn_swiglu: null pointer");
+    BF_CHECK_ARG(dtype != BF_DTYPE_BF16 || (aligned16(X) && aligned16(Wt) && aligned16(Vt) && aligned16(Ut) &&
+                                            aligned16(O) && aligned16(workspace)),
+                 "bf_rms_ffn_swiglu: bf16 buffers must be 16-byte aligned");
     require_sm100();
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == BF_DTYPE_BF16)
@@ -114,6 +121,8 @@ int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M, int64
                         void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     BF_CHECK_ARG(X && Yt && O, "bf_layernorm_matmul: null pointer");
+    BF_CHECK_ARG(dtype != BF_DTYPE_BF16 || (aligned16(X) && aligned16(Yt) && aligned16(O) && aligned16(workspace)),
+                 "bf_layernorm_matmul: bf16 buffers must be 16-byte aligned");
     require_sm100();
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == BF_DTYPE_BF16)
@@ -129,6 +138,8 @@ int bf_attention(const void* Q, const void* K, const void* Vt, void* O, int64_t 
                  int64_t D, int64_t Dv, int dtype, float scale, void* stream) {
   return guarded([&] {
     BF_CHECK_ARG(Q && K && Vt && O, "bf_attention: null pointer");
+    BF_CHECK_ARG(dtype != BF_DTYPE_BF16 || (aligned16(Q) && aligned16(K) && aligned16(Vt) && aligned16(O)),
+                 "bf_attention: bf16 buffers must be 16-byte aligned");
     require_sm100();
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == BF_DTYPE_BF16)

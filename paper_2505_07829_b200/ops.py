@@ -11,7 +11,8 @@ import torch
 from . import _lib
 from ._lib import BF_DTYPE_BF16, BF_DTYPE_F32, BF_FFN_FUSED, BF_FFN_TWO_PHASE, check
 
-_WS: dict[int, torch.Tensor] = {}
+# one cached workspace per (device, stream): calls on different streams may overlap
+_WS: dict[tuple[int, int], torch.Tensor] = {}
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -39,10 +40,11 @@ def _require(t: torch.Tensor, name: str, shape: tuple, dtype: torch.dtype, devic
 
 def _workspace(nbytes: int, device: torch.device) -> torch.Tensor:
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    ws = _WS.get(idx)
+    key = (idx, _stream_ptr(device))
+    ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-        _WS[idx] = ws
+        _WS[key] = ws
     return ws
 
 

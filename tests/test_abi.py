@@ -80,3 +80,16 @@ def test_sass_contains_tcgen05_and_tma():
     for mnem in ("UTCHMMA", "LDTM", "STTM", "UTMALDG", "UTMASTG"):
         assert mnem in sass, mnem
     assert "HMMA" not in sass.replace("UTCHMMA", "")
+
+
+def test_misaligned_bf16_buffers_rejected():
+    """Checked before any device query, so the error is the same with or without a GPU."""
+    lib = _lib.lib()
+    ok, bad = 1 << 20, (1 << 20) + 8
+    rc = lib.bf_layernorm_matmul(bad, ok, ok, 128, 64, 64, _lib.BF_DTYPE_BF16, 0.0, ok, 1 << 20, None)
+    assert rc == _lib.BF_ERR_INVALID_ARGUMENT
+    assert b"16-byte aligned" in lib.bf_last_error()
+    rc = lib.bf_attention(ok, ok, ok, bad, 1, 128, 128, 128, 128, _lib.BF_DTYPE_BF16, 0.0, None)
+    assert rc == _lib.BF_ERR_INVALID_ARGUMENT
+    rc = lib.bf_rms_ffn_swiglu(ok, ok, bad, ok, ok, 8, 8, 8, 8, _lib.BF_DTYPE_BF16, 0.0, 0, ok, 1 << 20, None)
+    assert rc == _lib.BF_ERR_INVALID_ARGUMENT
