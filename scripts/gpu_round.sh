@@ -15,3 +15,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_m
 fi
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
 true
+if [ "$FULL" = 1 ]; then
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:ffn_swiglu -s 1 -c 1 -o gpurun_out/prof_ffn70b -f python scripts/ncu_target.py ffn_70b fused 2 > gpurun_out/ncu_ffn70b.log 2>&1
+fi
