@@ -18,6 +18,7 @@ struct Params {
   float inv_d;
   float eps;
   int* flags;      // per m-tile count of finished gate/up tiles (fused mode)
+  int* wave;       // 2-SM kernel: tile iterations started, summed over clusters (wave sync), or null
 };
 
 struct Tile {

@@ -394,6 +394,7 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   p.inv_d = 1.0f / static_cast<float>(D);
   p.eps = eps;
   p.flags = flags;
+  p.wave = nullptr;
   // m-tiles per scheduling group: larger groups re-read the weights fewer times,
   // smaller groups keep the live part of H small enough to stay in L2.
   static const int group_env = [] {

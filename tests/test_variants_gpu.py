@@ -1,7 +1,8 @@
 """Parity of the non-default kernel variants that the environment selects (read once per
 process, hence the subprocesses): the 1-SM K1 and K2 kernels (BFGPU_FFN_1SM, BFGPU_LNMM_1SM),
-the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU) and non-default K1 scheduling groups
-(BFGPU_FFN_GROUP). Same oracle and tolerances as the default-path tests."""
+the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU), non-default K1/K2 scheduling groups
+(BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP) and the K1 wave sync switched off (BFGPU_FFN_WAVESYNC=0).
+Same oracle and tolerances as the default-path tests."""
 import os
 import subprocess
 import sys
@@ -49,6 +50,7 @@ print("ok")
         ("ffn", {"BFGPU_FFN_1SM": "1"}),
         ("ffn", {"BFGPU_FFN_GROUP": "1"}),
         ("ffn", {"BFGPU_FFN_GROUP": "64"}),
+        ("ffn", {"BFGPU_FFN_WAVESYNC": "0"}),
         ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
         ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
         ("attn", {"BFGPU_ATTN_EMU": "8"}),
