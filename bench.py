@@ -435,7 +435,7 @@ def run_ours(args, wl):
     if rank == 0:
         kernel_ms = ms_per_step  # one fused launch per step (fused schedule); per-rank device time
         achieved = inp["flops"] / (max_elapsed_ms / args.steps / 1e3) / 1e12
-        kkey = {"ffn": "ffn_swiglu_kernel", "lnmm": "ln_matmul_kernel", "attn": "attn_kernel"}[kind]
+        kkey = {"ffn": "ffn_swiglu_2sm_kernel", "lnmm": "ln_matmul_2sm_kernel", "attn": "attn_kernel"}[kind]
         capture = {"ffn": "prof_ffn" if args.schedule == "fused" else "prof_ffn2p", "lnmm": "prof_lnmm",
                    "attn": "prof_attn"}[kind]
         if wl["name"].startswith("C5"):
