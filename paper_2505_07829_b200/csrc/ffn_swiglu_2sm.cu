@@ -380,13 +380,18 @@ void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, cons
   };
   // flags (fused hand-off) and the statistics counter live together: one memset
   BF_CUDA(cudaMemsetAsync(flags, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
-  // Wave sync (on by default; BFGPU_FFN_WAVESYNC=0 disables). Measured, Llama-3-70B (C5):
-  // fused 948 -> 1160 TFLOP/s (SM clock under the power cap 817 -> 1050 MHz), DRAM per
-  // two-phase step 80+47 -> 40+38 GB; Llama-3-8B (C3): DRAM 3.16 -> 2.65 GB, speed unchanged.
-  static const bool wave_sync = [] {
+  // Wave sync (BFGPU_FFN_WAVESYNC=1 forces it on, 0 off; default: on for launches of at
+  // least 1e13 FLOP, i.e. the ones long enough to run into the board power cap). Measured,
+  // Llama-3-70B (C5, 4.6e13 FLOP): fused 948 -> 1160 TFLOP/s (SM clock under the power cap
+  // 817 -> 1050 MHz), DRAM per two-phase step 80+47 -> 40+38 GB. Llama-3-8B (C3, 2.9e12
+  // FLOP, 1.9 ms, below the cap): DRAM 3.16 -> 2.65 GB but 1.5% slower (fused 1479-1578 vs
+  // 1555-1561, two-phase 1555-1559 vs 1580-1582, three A/B pairs on one box).
+  static const int wave_env = [] {
     const char* v = std::getenv("BFGPU_FFN_WAVESYNC");
-    return !(v && v[0] == '0');
+    return v && v[0] ? (v[0] == '0' ? 0 : 1) : -1;
   }();
+  const double flops = 2.0 * p.M * static_cast<double>(p.F) * (2.0 * p.D + p.N);
+  const bool wave_sync = wave_env >= 0 ? wave_env == 1 : flops >= 1e13;
   p.wave = wave_sync ? stats_ready + 1 : nullptr;  // the spare int after the statistics counter
   if (schedule == BF_FFN_FUSED) {
     launch(kFused);

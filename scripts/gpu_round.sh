@@ -13,6 +13,7 @@ if [ "$FULL" = 1 ]; then
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_swiglu -s 2 -c 1 -o gpurun_out/prof_ffn -f python scripts/ncu_target.py ffn_8b fused 3 > gpurun_out/ncu_ffn.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_matmul -s 2 -c 1 -o gpurun_out/prof_lnmm -f python scripts/ncu_target.py lnmm fused 3 > gpurun_out/ncu_lnmm.log 2>&1
 fi
+[ "$FULL" = 1 ] && timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi.txt
 true
 if [ "$FULL" = 1 ]; then

@@ -1,7 +1,7 @@
 """Parity of the non-default kernel variants that the environment selects (read once per
 process, hence the subprocesses): the 1-SM K1 and K2 kernels (BFGPU_FFN_1SM, BFGPU_LNMM_1SM),
 the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU), non-default K1/K2 scheduling groups
-(BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP) and the K1 wave sync switched off (BFGPU_FFN_WAVESYNC=0).
+(BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP) and the K1 wave sync forced on at a size where it is off by default (BFGPU_FFN_WAVESYNC=1).
 Same oracle and tolerances as the default-path tests."""
 import os
 import subprocess
@@ -50,7 +50,7 @@ print("ok")
         ("ffn", {"BFGPU_FFN_1SM": "1"}),
         ("ffn", {"BFGPU_FFN_GROUP": "1"}),
         ("ffn", {"BFGPU_FFN_GROUP": "64"}),
-        ("ffn", {"BFGPU_FFN_WAVESYNC": "0"}),
+        ("ffn", {"BFGPU_FFN_WAVESYNC": "1"}),
         ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
         ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
         ("attn", {"BFGPU_ATTN_EMU": "8"}),
