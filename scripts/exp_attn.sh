@@ -1,3 +1,4 @@
 #!/bin/bash
-for e in 8 12; do echo "split EMU=$e $(TRACE_GAUSS=1 ./scripts/micro/attn_trace_$e | head -1)"; echo "noxch EMU=$e $(TRACE_GAUSS=1 ./scripts/micro/attn_noxch_$e | head -1)"; done
-TRACE_GAUSS=1 ./scripts/micro/attn_noxch_8 | sed -n 8,14p
+timeout 300 python -m pytest tests/test_attention_gpu.py -x -q 2>&1 | tail -1
+for r in 1 2; do for e in 8 12; do echo "EMU=$e"; BFGPU_ATTN_EMU=$e timeout 120 python scripts/quick_perf.py attn 2>&1 | grep -v "^$"; done; done
+TRACE_GAUSS=1 ./scripts/micro/attn_trace_8 | sed -n 1,16p

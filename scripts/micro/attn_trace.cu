@@ -50,22 +50,22 @@ int main() {
   std::vector<unsigned long long> t(4 * 64 * 8);
   cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long base = t[(0 * 64 + 10) * 8 + 0];
-  printf("blk | WG0: wait  S_ready  loaded  exp_done  arrived | WG1: same | MMA tile0: p_seen token pv_h0h1 mmas_issued commits_done | tile1: same\n");
-  printf("MMA waits: tile0 p_seen tma_ok (unused) token | tile1 same\n");
-  for (int g = 16; g < 22; ++g) {
-    auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + g) * 8 + k] - base); };
-    printf("%3d | %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld\n", g, v(2, 0), v(2, 5), v(2, 6), v(2, 2), v(3, 0),
-           v(3, 5), v(3, 6), v(3, 2));
-  }
-  printf("epilogue of the tile ending at block 15 (WG0 | WG1): enter o_full_seen after_half(last)\n");
-  {
-    auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + 15) * 8 + k] - base); };
-    printf("    %6lld %6lld %6lld | %6lld %6lld %6lld\n", v(0, 5), v(0, 6), v(0, 7), v(1, 5), v(1, 6), v(1, 7));
-  }
+  printf("softmax (warp 0) per sub-tile: wait S_ready max_done half0_arrived half1_arrived | MMA issuer i: p_seen token pv_issued qk_issued commits_done\n");
   for (int g = 10; g < 22; ++g) {
     auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + g) * 8 + k] - base); };
-    printf("%3d | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld %6lld\n",
+    printf("%3d | T0 %6lld %6lld %6lld %6lld %6lld | T1 %6lld %6lld %6lld %6lld %6lld | M0 %6lld %6lld %6lld %6lld %6lld | M1 %6lld %6lld %6lld %6lld %6lld\n",
            g, v(0, 0), v(0, 1), v(0, 2), v(0, 3), v(0, 4), v(1, 0), v(1, 1), v(1, 2), v(1, 3), v(1, 4), v(2, 0), v(2, 2),
            v(2, 3), v(2, 4), v(2, 1), v(3, 0), v(3, 2), v(3, 3), v(3, 4), v(3, 1));
+  }
+#ifdef BF_ATTN_TRACE_LD
+  for (int g = 16; g < 22; ++g) {
+    auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + g) * 8 + k] - base); };
+    printf("%3d S_ready->loaded->max: T0 %lld %lld | T1 %lld %lld\n", g, v(0, 5) - v(0, 1), v(0, 2) - v(0, 5), v(1, 5) - v(1, 1), v(1, 2) - v(1, 5));
+  }
+#endif
+  printf("epilogue warpgroup, second tile (T0 | T1): enter o_full_seen stored\n");
+  {
+    auto v = [&](int slot, int k) { return (long long)(t[(slot * 64 + 1) * 8 + k] - base); };
+    printf("    %6lld %6lld %6lld | %6lld %6lld %6lld\n", v(0, 5), v(0, 6), v(0, 7), v(1, 5), v(1, 6), v(1, 7));
   }
 }

@@ -53,7 +53,7 @@ print("ok")
         ("ffn", {"BFGPU_FFN_WAVESYNC": "1"}),
         ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
         ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
-        ("attn", {"BFGPU_ATTN_EMU": "8"}),
+        ("attn", {"BFGPU_ATTN_EMU": "0"}),
         ("attn", {"BFGPU_ATTN_EMU": "12"}),
         ("attn", {"BFGPU_ATTN_EMU": "16"}),
     ],
