@@ -63,7 +63,10 @@ def test_golden_fp32_mode(torch_ops, fixture):
 @pytest.mark.parametrize(
     "BH,Sq,Skv,D,Dv",
     [(1, 128, 128, 128, 128), (3, 200, 328, 128, 128), (2, 64, 1000, 64, 64), (2, 300, 256, 128, 64),
-     (4, 512, 512, 64, 128)],
+     (4, 512, 512, 64, 128),
+     # more tiles than SMs: several tiles per persistent CTA, the next tile's first QK issued
+     # with the last PV; single-block tiles and ragged last blocks
+     (400, 256, 128, 128, 128), (200, 300, 200, 64, 64)],
 )
 def test_shapes_vs_oracle(torch_ops, BH, Sq, Skv, D, Dv):
     torch, ops = torch_ops
