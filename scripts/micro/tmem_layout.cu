@@ -21,14 +21,16 @@ __global__ void layout(uint32_t* out) {
   tmem_wait_st();
   __syncwarp();
   if (warp == 0) {
-    uint32_t a, b0, b1, d0, d1, d2, d3, e0, e1;
+    uint32_t a, b0, b1, d0, d1, d2, d3, e0, e1, f0, f1;
     asm volatile("tcgen05.ld.sync.aligned.16x64b.x1.b32 {%0}, [%1];" : "=r"(a) : "r"(tmem));
     asm volatile("tcgen05.ld.sync.aligned.16x128b.x1.b32 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(tmem));
     asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3) : "r"(tmem));
     asm volatile("tcgen05.ld.sync.aligned.16x64b.x2.b32 {%0, %1}, [%2];" : "=r"(e0), "=r"(e1) : "r"(tmem + (16u << 16)));
+    asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x2.b32 {%0, %1}, [%2], 4;" : "=r"(f0), "=r"(f1) : "r"(tmem));
     tmem_wait_ld();
     uint32_t* o = out + lane * 16;
+    o[9] = f0; o[10] = f1;
     o[0] = a; o[1] = b0; o[2] = b1; o[3] = d0; o[4] = d1; o[5] = d2; o[6] = d3; o[7] = e0; o[8] = e1;
   }
   tc_fence_before(); __syncthreads();
@@ -40,8 +42,8 @@ int main() {
   layout<<<1, 128>>>(d);
   uint32_t h[32 * 16]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
-  const char* names[9] = {"16x64b.x1", "16x128b[0]", "16x128b[1]", "16x256b[0]", "16x256b[1]", "16x256b[2]", "16x256b[3]", "16x64b.x2@16[0]", "16x64b.x2@16[1]"};
-  for (int k = 0; k < 9; ++k) {
+  const char* names[11] = {"16x64b.x1", "16x128b[0]", "16x128b[1]", "16x256b[0]", "16x256b[1]", "16x256b[2]", "16x256b[3]", "16x64b.x2@16[0]", "16x64b.x2@16[1]", "16x32bx2.x2,4[0]", "16x32bx2.x2,4[1]"};
+  for (int k = 0; k < 11; ++k) {
     printf("%-16s", names[k]);
     for (int t = 0; t < 32; ++t) printf(" %u:%u", h[t * 16 + k] >> 8, h[t * 16 + k] & 255);
     printf("\n");
