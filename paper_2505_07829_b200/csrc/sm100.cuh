@@ -71,14 +71,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 // Blocking wait on the phase with the given parity. A watchdog traps after
-// ~20 s so a pipeline bug surfaces as a launch error instead of a hung GPU.
+// ~20 s so a pipeline bug surfaces as a launch error instead of a hung GPU; the timer is
+// only read every 64 unsuccessful waits (reading it on every poll made the wait loops
+// ~100 M of K2's 245 M warp instructions, ncu source page). A try_wait suspend-time hint
+// (0x989680 ns) was tried instead and slowed K3 by 5%: waiters woke late.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  if (mbar_try_wait(addr, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+    if ((++spins & 63u) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > 20000000000ull) {
+        __trap();
+      }
+    }
   }
 }
 
@@ -435,11 +444,17 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  if (mbar_try_wait_cluster(addr, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try_wait_cluster(addr, parity)) {
-    if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+    if ((++spins & 63u) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > 20000000000ull) {
+        __trap();
+      }
+    }
   }
 }
 
