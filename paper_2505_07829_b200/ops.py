@@ -139,3 +139,79 @@ def attention(Q, K, Vt, scale: float | None = None, out=None):
 
 def kernel_launches() -> int:
     return int(_lib.lib().bf_kernel_launches())
+
+
+# ----------------------------------------------------------------- host-buffer calls
+# The reference's execute() receives host matrices. from_host() is that call shape on the
+# GPU: inputs in pinned host memory, output back into pinned host memory, with the copies
+# overlapped with the kernels. Shared operands (weights) go first on an H2D stream; the
+# row-sharded operands follow in `chunks` slices along dim 0 (rows, or heads for attention),
+# each slice's kernel starts as soon as its slice has landed, and each slice's output
+# leaves on a D2H stream while the next slice computes. Rows are independent in all three
+# block programs (per-row statistics / per-head attention), so slicing is exact.
+_SIDE_STREAMS: dict[tuple[int, str], torch.cuda.Stream] = {}
+_HOST_BUFS: dict[tuple, torch.Tensor] = {}
+
+
+def _side_stream(device: torch.device, name: str) -> torch.cuda.Stream:
+    key = (device.index, name)
+    s = _SIDE_STREAMS.get(key)
+    if s is None:
+        s = torch.cuda.Stream(device=device)
+        _SIDE_STREAMS[key] = s
+    return s
+
+
+def _device_like(t: torch.Tensor, device: torch.device, tag: str) -> torch.Tensor:
+    key = (device.index, tag, tuple(t.shape), t.dtype)
+    b = _HOST_BUFS.get(key)
+    if b is None:
+        b = torch.empty(t.shape, dtype=t.dtype, device=device)
+        _HOST_BUFS[key] = b
+    return b
+
+
+def from_host(fn, row_inputs, shared_inputs, out_host, chunks: int = 4, **kwargs):
+    """out_host = fn(*row_inputs, *shared_inputs) for pinned host tensors, copies overlapped.
+
+    fn is one of rms_ffn_swiglu / layernorm_matmul / attention. Its row-sharded operands are
+    `row_inputs` (sliced along dim 0), the rest `shared_inputs` (copied whole), in fn's
+    argument order: row operands first. Returns out_host; the current stream is ordered
+    after the last device-to-host copy.
+    """
+    for t in (*row_inputs, *shared_inputs, out_host):
+        if t.is_cuda:
+            raise ValueError("from_host takes host tensors")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comp = torch.cuda.current_stream(dev)
+    h2d, d2h = _side_stream(dev, "h2d"), _side_stream(dev, "d2h")
+    rows = row_inputs[0].shape[0]
+    chunks = max(1, min(chunks, rows))
+    bounds = [rows * k // chunks for k in range(chunks + 1)]
+    row_dev = [_device_like(t, dev, f"row{i}") for i, t in enumerate(row_inputs)]
+    shared_dev = [_device_like(t, dev, f"shared{i}") for i, t in enumerate(shared_inputs)]
+    out_dev = _device_like(out_host, dev, "out")
+    h2d.wait_stream(comp)  # the previous call's kernels are done with the device buffers
+    d2h.wait_stream(comp)
+    ev_in = [torch.cuda.Event() for _ in range(chunks)]
+    ev_out = [torch.cuda.Event() for _ in range(chunks)]
+    with torch.cuda.stream(h2d):
+        for h, d in zip(shared_inputs, shared_dev):
+            d.copy_(h, non_blocking=True)
+        for k in range(chunks):
+            a, b = bounds[k], bounds[k + 1]
+            for h, d in zip(row_inputs, row_dev):
+                d[a:b].copy_(h[a:b], non_blocking=True)
+            ev_in[k].record(h2d)
+    for k in range(chunks):
+        a, b = bounds[k], bounds[k + 1]
+        comp.wait_event(ev_in[k])
+        fn(*[d[a:b] for d in row_dev], *shared_dev, out=out_dev[a:b], **kwargs)
+        ev_out[k].record(comp)
+    with torch.cuda.stream(d2h):
+        for k in range(chunks):
+            a, b = bounds[k], bounds[k + 1]
+            d2h.wait_event(ev_out[k])
+            out_host[a:b].copy_(out_dev[a:b], non_blocking=True)
+    comp.wait_stream(d2h)
+    return out_host
