@@ -80,8 +80,10 @@ class ClockSampler:
 
     def __init__(self, device_index: int, interval_s: float = 0.005):
         self.samples: list[int] = []
+        self.power_w: list[float] = []
         self.reasons: set[str] = set()
         self.max_mhz = None
+        self.power_limit_w = None
         self._stop = threading.Event()
         self._ok = False
         try:
@@ -91,6 +93,10 @@ class ClockSampler:
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1000.0
+            except Exception:
+                self.power_limit_w = None
             self._ok = True
         except Exception:
             self._ok = False
@@ -102,6 +108,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.power_w.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
@@ -125,7 +132,8 @@ class ClockSampler:
         if not self._ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_max": max(self.power_w) if self.power_w else None, "power_limit_w": self.power_limit_w}
 
 
 def unfused_measured(kind: str):
