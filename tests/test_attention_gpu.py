@@ -66,7 +66,10 @@ def test_golden_fp32_mode(torch_ops, fixture):
      (4, 512, 512, 64, 128),
      # more tiles than SMs: several tiles per persistent CTA, the next tile's first QK issued
      # with the last PV; single-block tiles and ragged last blocks
-     (400, 256, 128, 128, 128), (200, 300, 200, 64, 64)],
+     (400, 256, 128, 128, 128), (200, 300, 200, 64, 64),
+     # a single valid key block smaller than one key half (Skv = 8), and one ending 8 keys into
+     # the second half (72); a single query row
+     (3, 130, 8, 128, 128), (2, 257, 72, 64, 64), (5, 1, 136, 128, 64)],
 )
 def test_shapes_vs_oracle(torch_ops, BH, Sq, Skv, D, Dv):
     torch, ops = torch_ops
