@@ -485,7 +485,7 @@ def run_ours(args, wl):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms, "chunks": e2e_chunks,
-                    "path": "ops.from_host -> C-ABI bf_*: pinned host buffers, every input H2D and the output D2H inside each step, overlapped with the kernels in row slices"},
+                    "path": "ops.from_host -> C-ABI bf_*: pinned host buffers, every input H2D and the output D2H inside each step, overlapped with the kernels in row slices; consecutive steps alternate two device buffer sets"},
             "gpu_launches": launches,
             "step_ms_median": statistics.median(per_step),
             "clocks": clk.summary(),

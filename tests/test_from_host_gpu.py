@@ -54,3 +54,20 @@ def test_from_host_rejects_device_tensors():
     X = torch.zeros(4, 4, device="cuda")
     with pytest.raises(ValueError, match="host tensors"):
         ops.from_host(ops.layernorm_matmul, [X], [], torch.zeros(4, 4))
+
+
+def test_back_to_back_calls_alternate_buffers_safely():
+    """Consecutive calls reuse two device buffer sets; each call's output must be its own."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, K, N = 640, 256, 384
+    Yt = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    Xs = [torch.randn(M, K, device="cuda", generator=g).bfloat16() for _ in range(5)]
+    refs = [ops.layernorm_matmul(X, Yt).cpu() for X in Xs]
+    hosts = [_pinned(X) for X in Xs]
+    Yh = _pinned(Yt)
+    outs = [torch.empty(M, N, dtype=torch.bfloat16).pin_memory() for _ in Xs]
+    for Xh, o in zip(hosts, outs):
+        ops.from_host(ops.layernorm_matmul, [Xh], [Yh], o, chunks=3)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
