@@ -401,11 +401,17 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
     const char* v = std::getenv("BFGPU_FFN_GROUP");
     return v ? std::atoi(v) : 0;
   }();
-  // Default: 32 m-tiles (4096 rows) per group. Measured (TFLOP/s, fused, 2-SM):
-  //   Llama-3-8B  (C3): g=16 1470, g=32 1581, g=64 1477 (1-SM: 1226 / 1304 / 1417 / 1251 at 8/16/32/64)
-  //   Llama-3-70B (C5, power-capped): g=16 941-964, g=32 1016, g=64 1000-1024, g=128 983
+  // Default: 32 m-tiles (4096 rows) per group, 16 (2048 rows) for launches of at least
+  // 1e13 FLOP, which run power-capped with the 2-SM kernel's wave sync on (same threshold,
+  // ffn_swiglu_2sm.cu). Measured (TFLOP/s, fused, 2-SM):
+  //   Llama-3-8B  (C3): g=16 1470, g=32 1581, g=64 1477 (1-SM: 1226 / 1304 / 1417 / 1251 at 8/16/32/64);
+  //     again with the final kernel, alternating: g=32 1542-1565, g=24 1509, g=16 1483-1493
+  //   Llama-3-70B (C5, power-capped), before the wave sync: g=16 941-964, g=32 1016,
+  //     g=64 1000-1024, g=128 983; with it, alternating runs: g=16 1267-1279, g=32 1212-1265,
+  //     g=8 1204, g=64 1122, g=128 1052 (scripts/exp_70b_group.sh)
   // Smaller groups re-read the weights more often; larger ones let H and X thrash L2.
-  const int g2 = 32;
+  const double flops = 2.0 * static_cast<double>(M) * static_cast<double>(F) * (2.0 * D + N);
+  const int g2 = flops >= 1e13 ? 16 : 32;
   p.group = group_env > 0 ? group_env : std::min(g2, p.Mt);
 
   // CTA-pair path (default): 256-row m-units, B split across the pair.
