@@ -19,6 +19,8 @@ struct Params {
   float eps;
   int* flags;      // per m-tile count of finished gate/up tiles (fused mode)
   int* wave;       // 2-SM kernel: tile iterations started, summed over clusters (wave sync), or null
+  int* seg;        // 2-SM fused kernel: tiles of the first two gate/up segments started (segment sync), or null
+  int seg_tiles;   // ... their count: tiles [0, seg_tiles) of the fused order
 };
 
 struct Tile {

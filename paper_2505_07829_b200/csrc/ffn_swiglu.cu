@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 namespace {
 
 size_t ffn_h_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 2, 1024); }
-size_t ffn_flag_bytes(int64_t M) { return align_up(static_cast<size_t>((M + 127) / 128 + 2) * 4, 256); }
+size_t ffn_flag_bytes(int64_t M) { return align_up(static_cast<size_t>((M + 127) / 128 + 3) * 4, 256); }
 size_t ffn_rstat_bytes(int64_t M) { return align_up(static_cast<size_t>(M) * 4, 256); }
 
 }  // namespace
@@ -395,6 +395,8 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   p.eps = eps;
   p.flags = flags;
   p.wave = nullptr;
+  p.seg = nullptr;
+  p.seg_tiles = 0;
   // m-tiles per scheduling group: larger groups re-read the weights fewer times,
   // smaller groups keep the live part of H small enough to stay in L2.
   static const int group_env = [] {

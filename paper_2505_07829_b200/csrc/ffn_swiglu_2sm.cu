@@ -120,6 +120,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++iter) {
         const Tile tl = ffn::decode_tile(p, t);
         const int mrow = tl.m * 2 * BM + static_cast<int>(rank) * BM;
+        if (p.seg && leader) {
+          // Segment sync (fused schedule without the wave sync): no cluster starts a tile past
+          // the first two gate/up segments until all of those have been started, so the
+          // down-projection segments begin with the clusters aligned, as after a kernel
+          // boundary. Tiles before that point never wait here.
+          if (t < p.seg_tiles) {
+            red_release_gpu_add(p.seg, 1);
+          } else if (t - num_clusters < p.seg_tiles) {  // this cluster's first tile past the point
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_gpu(p.seg) < p.seg_tiles) {
+              __nanosleep(64);
+              if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+            }
+          }
+        }
         if (p.wave && leader) {
           // Wave sync: start iteration i only once every cluster has started iteration i-1,
           // so the tiles of one wave (consecutive indices, which share operand row-blocks)
@@ -372,7 +387,7 @@ void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, cons
     BF_CHECK_ARG(tiles < (1ll << 31), "bf_rms_ffn_swiglu: too many tiles");
     q.num_tiles = static_cast<int>(tiles);
     const int clusters = static_cast<int>(std::min<long long>(tiles, sms / 2));
-    if (q.wave) BF_CUDA(cudaMemsetAsync(q.wave, 0, sizeof(int), stream));
+    if (q.wave || q.seg) BF_CUDA(cudaMemsetAsync(stats_ready + 1, 0, 2 * sizeof(int), stream));
     ffn_swiglu_2sm_kernel<<<clusters * 2, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_wt, tm_vt, tm_ut_half, tm_h,
                                                                            tm_o, q, ex);
     BF_CUDA(cudaGetLastError());
@@ -393,6 +408,19 @@ void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, cons
   const double flops = 2.0 * p.M * static_cast<double>(p.F) * (2.0 * p.D + p.N);
   const bool wave_sync = wave_env >= 0 ? wave_env == 1 : flops >= 1e13;
   p.wave = wave_sync ? stats_ready + 1 : nullptr;  // the spare int after the statistics counter
+  // Segment sync for the fused schedule when the wave sync is off (BFGPU_FFN_SEGSYNC=0 disables).
+  static const bool seg_env = [] {
+    const char* v = std::getenv("BFGPU_FFN_SEGSYNC");
+    return !(v && v[0] == '0');
+  }();
+  p.seg = nullptr;
+  p.seg_tiles = 0;
+  if (schedule == BF_FFN_FUSED && !wave_sync && seg_env) {
+    const int ngroups = (p.Mt + p.group - 1) / p.group;
+    const int g0 = std::min(p.group, p.Mt), g1 = ngroups > 1 ? std::min(p.group, p.Mt - p.group) : 0;
+    p.seg = stats_ready + 2;
+    p.seg_tiles = (g0 + g1) * p.Ft;
+  }
   if (schedule == BF_FFN_FUSED) {
     launch(kFused);
   } else {
