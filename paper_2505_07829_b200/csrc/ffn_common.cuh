@@ -21,6 +21,7 @@ struct Params {
   int* wave;       // 2-SM kernel: tile iterations started, summed over clusters (wave sync), or null
   int* seg;        // 2-SM fused kernel: tiles of the first two gate/up segments started (segment sync), or null
   int seg_tiles;   // ... their count: tiles [0, seg_tiles) of the fused order
+  int braster;     // down-projection tiles: m-units per raster block (0: m fastest over the whole group)
 };
 
 struct Tile {
@@ -56,7 +57,19 @@ __device__ __forceinline__ Tile decode_tile(const Params& p, int t) {
     }
     const int gs = group_size(p, g);
     const int cnt = gs * (kind == 0 ? p.Ft : p.Nt);
-    if (t < cnt) return Tile{kind, g * p.group + t % gs, t / gs};
+    if (t < cnt) {
+      if (kind == 1 && p.braster > 0 && gs > p.braster) {
+        // blocks of braster m-units, n-chunks in order, m fastest inside a block: a wave of
+        // down tiles then reads H for braster m-units and Ut for a few n-chunks, instead of
+        // H for the whole group
+        for (int mb = 0;; mb += p.braster) {
+          const int bsz = min(p.braster, gs - mb);
+          if (t < bsz * p.Nt) return Tile{1, g * p.group + mb + t % bsz, t / bsz};
+          t -= bsz * p.Nt;
+        }
+      }
+      return Tile{kind, g * p.group + t % gs, t / gs};
+    }
     t -= cnt;
   }
   return Tile{-1, 0, 0};

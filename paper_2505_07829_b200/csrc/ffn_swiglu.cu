@@ -397,6 +397,15 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   p.wave = nullptr;
   p.seg = nullptr;
   p.seg_tiles = 0;
+  // Down-projection raster (BFGPU_FFN_BRASTER, m-units of 256 rows per block; 0 = off).
+  // CTA-pair default 8, measured at C3 (ncu DRAM read per launch; 2 s sustained TFLOP/s):
+  //   fused 1.99 GB (off) / 1.83 GB (8) / 2.06 GB (4); two-phase down launch 1.22 / 1.09 / 1.23;
+  //   sustained fused 1306 (off) vs 1313-1316 (8). scripts/exp_braster.sh
+  static const int braster_env = [] {
+    const char* v = std::getenv("BFGPU_FFN_BRASTER");
+    return v ? std::atoi(v) : -1;
+  }();
+  p.braster = 0;
   // m-tiles per scheduling group: larger groups re-read the weights fewer times,
   // smaller groups keep the live part of H small enough to stay in L2.
   static const int group_env = [] {
@@ -425,6 +434,7 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
     Params q = p;
     q.Mt = static_cast<int>((M + 2 * BM - 1) / (2 * BM));
     q.group = std::max(1, p.group / 2);
+    q.braster = braster_env >= 0 ? braster_env : 8;
     const CUtensorMap tm_ut_half = make_tmap_bf16(Ut, N, F, F, BK, 128);
     ffn_swiglu_bf16_2sm(tm_x, tm_wt, tm_vt, tm_ut_half, tm_h, tm_o, q, schedule, flags, X, rstat,
                         flags + q.Mt * 2, stream);

@@ -52,6 +52,8 @@ print("ok")
         ("ffn", {"BFGPU_FFN_GROUP": "64"}),
         ("ffn", {"BFGPU_FFN_WAVESYNC": "1"}),
         ("ffn", {"BFGPU_FFN_SEGSYNC": "0"}),
+        ("ffn", {"BFGPU_FFN_BRASTER": "0"}),
+        ("ffn", {"BFGPU_FFN_BRASTER": "3"}),
         ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
         ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
         ("attn", {"BFGPU_ATTN_EMU": "0"}),
