@@ -399,9 +399,10 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 }
 
 // 2^x for a pair on the FMA pipe (offloads MUFU.EX2): x = j + f with j = rint(x)
-// from the 1.5*2^23 rounding trick, 2^f on [-1/2, 1/2] by a degree-3 polynomial
-// fitted for minimax relative error (7.5e-5, far below the bf16 rounding of P),
-// and j added into the exponent field. Inputs are clamped at -126 so masked
+// from the 1.5*2^23 rounding trick, 2^f on [-1/2, 1/2] by a degree-2 polynomial
+// fitted for minimax relative error (1.7e-3, below the 2^-9 bf16 rounding of P; the
+// degree-3 fit, 7.5e-5, cost one more FFMA2 per pair and 1.5% of K3's speed at C2,
+// scripts/exp_poly.sh), and j added into the exponent field. Inputs are clamped at -126 so masked
 // (-inf) or far-below-max scores give ~2^-126 instead of a wrapped exponent
 // (at j = -127 a p < 1 would carry the exponent field into the sign bit).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
@@ -411,9 +412,8 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 t = fadd2(x, make_float2(kRound, kRound));
   const float2 j = fadd2(t, make_float2(-kRound, -kRound));
   const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);
-  float2 p = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
-  p = ffma2(p, f, make_float2(0.69326097f, 0.69326097f));
-  p = ffma2(p, f, make_float2(0.9999281f, 0.9999281f));
+  float2 p = ffma2(make_float2(0.2384257f, 0.2384257f), f, make_float2(0.70344281f, 0.70344281f));
+  p = ffma2(p, f, make_float2(1.00044296f, 1.00044296f));
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
