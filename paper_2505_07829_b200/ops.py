@@ -228,3 +228,10 @@ def from_host(fn, row_inputs, shared_inputs, out_host, chunks: int = 4, **kwargs
             out_host[a:b].copy_(out_dev[a:b], non_blocking=True)
     comp.wait_stream(d2h)
     return out_host
+
+
+def clear_host_buffers() -> None:
+    """Free the device buffers from_host() keeps per (shapes, dtypes) between calls."""
+    torch.cuda.synchronize()
+    _HOST_BUFS.clear()
+    _SLOTS.clear()

@@ -71,3 +71,8 @@ def test_back_to_back_calls_alternate_buffers_safely():
     torch.cuda.synchronize()
     for o, r in zip(outs, refs):
         assert torch.equal(o, r)
+    ops.clear_host_buffers()
+    o = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    ops.from_host(ops.layernorm_matmul, [hosts[0]], [Yh], o, chunks=2)
+    torch.cuda.synchronize()
+    assert torch.equal(o, refs[0])
