@@ -235,6 +235,41 @@ def step_fn(wl, inp, schedule, out):
     return lambda: ops.attention(inp["Q"], inp["K"], inp["Vt"], out=out)
 
 
+def check_output(wl, inp, out) -> dict:
+    """Validate the timed output: stratified rows (one per 256-row m-unit) or heads against an
+    fp32 torch reference on the device, same bf16 inputs, TF32 off (tests/torch_ref.py)."""
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch_ref
+    from helpers import DeviceErr
+
+    kind = wl["kind"]
+    err = DeviceErr()
+    if kind in ("ffn", "lnmm"):
+        rows = torch.arange(0, inp["rows"], 256, device=out.device)
+        rows = torch.clamp(rows + torch.randint(0, 256, rows.shape, device=out.device, generator=torch.Generator(
+            device=out.device).manual_seed(5)), max=inp["rows"] - 1)
+        if kind == "ffn":
+            gen = torch_ref.rms_ffn_swiglu_chunks(inp["X"][rows], inp["Wt"], inp["Vt"], inp["Ut"])
+        else:
+            gen = torch_ref.layernorm_matmul_chunks(inp["X"][rows], inp["Yt"])
+        for sl, ref in gen:
+            err.add(out[rows][sl], ref)
+        what = f"{rows.numel()} rows, one per 256-row m-unit"
+        tol = 1e-2
+    else:
+        heads = torch.arange(0, inp["rows"], max(1, inp["rows"] // 16), device=out.device)
+        for sl, ref in torch_ref.attention_chunks(inp["Q"][heads], inp["K"][heads], inp["Vt"][heads]):
+            err.add(out[heads][sl], ref)
+        what = f"{heads.numel()} heads of {inp['rows']}"
+        tol = 2e-2
+    s = err.summary()
+    s["pass"] = bool(s["nonfinite"] == 0 and s["rel"] <= 2e-2 and s["excess"] <= tol)
+    s["sample"] = what + ", vs fp32 torch reference on the same bf16 inputs"
+    return s
+
+
 # ------------------------------------------------------------------ CPU reference
 def reference_session(wl: dict, inp_shapes: dict, threads: int | None = None, shard_rows: int | None = None):
     """Build a row-sharded reference-executor session for the workload (rank 0, host)."""
@@ -432,6 +467,16 @@ def run_ours(args, wl):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev) / e2e_steps
     e2e_value = total_flops / (e2e_ms / 1e3) / 1e12
 
+    check = check_output(wl, inp, out) if not args.no_check else None
+    plan = None
+    try:
+        dims = {"ffn": lambda: (inp["rows"], wl["D"], wl["F"], wl["N"]), "lnmm": lambda: (inp["rows"], wl["K"], wl["N"]),
+                "attn": lambda: (inp["rows"], wl["S"], wl["S"], wl["Dh"], wl["Dh"])}[kind]()
+        pattern = {"ffn": "rms_ffn_swiglu", "lnmm": "layernorm_matmul", "attn": "attention"}[kind]
+        plan = ops.plan(pattern, dims, schedule=args.schedule if kind == "ffn" else "fused", device=dev)
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        plan = {"error": str(e)}
+
     # ---- reference-model traffic (the reference's own traffic_bytes, metrics.hpp:154)
     model = None
     try:
@@ -500,6 +545,8 @@ def run_ours(args, wl):
                     "ms_per_step": e2e_ms, "chunks": e2e_chunks,
                     "path": "ops.from_host -> C-ABI bf_*: pinned host buffers, every input H2D and the output D2H inside each step, overlapped with the kernels in row slices; consecutive steps alternate two device buffer sets"},
             "gpu_launches": launches,
+            "check": check,
+            "plan": plan,
             "step_ms_median": statistics.median(per_step),
             "clocks": clk.summary(),
         }
@@ -518,6 +565,7 @@ def main(argv=None):
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="ffn_8b")
     ap.add_argument("--schedule", choices=["fused", "two_phase"], default="fused")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip validating sampled rows of the timed output")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     wl = WORKLOADS[args.workload]

@@ -162,6 +162,24 @@ BF_API int bf_copy_to_host(void* dst, const void* src, size_t bytes, void* strea
 BF_API int bf_stream_synchronize(void* stream);
 
 /* ------------------------------------------------------------------------
+ * Device memory / tile planner
+ *   How a launch of a fused program maps onto the device: which kernel, the
+ *   tile and SMEM stage ring, TMEM columns, grid and co-resident capacity,
+ *   scheduling group (the L2-resident slab), cross-cluster sync, and why.
+ *   The reference has no counterpart (its executor walks Eigen blocks,
+ *   interpreter.hpp:319-371); the plan is the B200 reading of the fused
+ *   program's map nests and port modes (ir.hpp:126-154, 265-276).
+ * dims: RMS_FFN_SWIGLU {M, D, F, N}; LAYERNORM_MATMUL {M, K, N};
+ *       ATTENTION {BH, Sq, Skv, D, Dv}. Writes a NUL-terminated JSON object.
+ * Needs a device (the plan reads its SM count, SMEM, L2 and occupancy).
+ * ---------------------------------------------------------------------- */
+#define BF_PATTERN_RMS_FFN_SWIGLU 0
+#define BF_PATTERN_LAYERNORM_MATMUL 1
+#define BF_PATTERN_ATTENTION 2
+BF_API int bf_plan_json(int pattern, const int64_t* dims, int ndims, int dtype, int schedule, char* buf,
+                        size_t len);
+
+/* ------------------------------------------------------------------------
  * Introspection
  * ---------------------------------------------------------------------- */
 BF_API const char* bf_last_error(void);

@@ -26,6 +26,10 @@ BF_DTYPE_F32 = 1
 BF_FFN_FUSED = 0
 BF_FFN_TWO_PHASE = 1
 
+BF_PATTERN_RMS_FFN_SWIGLU = 0
+BF_PATTERN_LAYERNORM_MATMUL = 1
+BF_PATTERN_ATTENTION = 2
+
 # (name, restype, argtypes) for every symbol declared in include/bfgpu.h
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p
@@ -61,6 +65,8 @@ _SIGNATURES = [
     ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_copy_to_host", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_stream_synchronize", ctypes.c_int, [_vp]),
+    ("bf_plan_json", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_i64), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_char_p, ctypes.c_size_t]),
     ("bf_last_error", ctypes.c_char_p, []),
     ("bf_version", ctypes.c_int, []),
     ("bf_kernel_launches", ctypes.c_uint64, []),

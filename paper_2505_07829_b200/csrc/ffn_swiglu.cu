@@ -36,6 +36,7 @@
 #include "sm100.cuh"
 #include "tma_host.hpp"
 #include "ffn_common.cuh"
+#include "plan.hpp"
 
 namespace bfgpu {
 namespace ffn {
@@ -338,10 +339,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 
+KernelSpec ffn1_spec() {
+  using namespace ffn;
+  KernelSpec k;
+  k.name = "ffn_swiglu_kernel";
+  k.func = reinterpret_cast<const void*>(&ffn_swiglu_kernel);
+  k.threads = NUM_THREADS;
+  k.smem_bytes = SMEM_BYTES;
+  k.tmem_cols = TMEM_COLS;
+  k.cluster = 1;
+  k.tile_m = BM;
+  k.tile_n = BN;
+  k.tile_k = BK;
+  k.stages = STAGES;
+  k.grid_sync = true;  // fused down tiles wait on other CTAs' gate/up tiles
+  return k;
+}
+
 namespace {
 
 size_t ffn_h_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 2, 1024); }
-size_t ffn_flag_bytes(int64_t M) { return align_up(static_cast<size_t>((M + 127) / 128 + 3) * 4, 256); }
+// Counters: per m-tile completion flags (ceil(M/128) for the 1-SM kernel, 2*ceil(M/256) for
+// the CTA pair, which can be one more), then the statistics, wave and segment counters.
+size_t ffn_flag_count(int64_t M) { return std::max((M + 127) / 128, 2 * ((M + 255) / 256)) + 3; }
+size_t ffn_flag_bytes(int64_t M) { return align_up(ffn_flag_count(M) * 4, 256); }
 size_t ffn_rstat_bytes(int64_t M) { return align_up(static_cast<size_t>(M) * 4, 256); }
 
 }  // namespace
@@ -352,11 +373,8 @@ size_t ffn_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
   return ffn_h_bytes(M, F) + ffn_rstat_bytes(M) + ffn_flag_bytes(M);
 }
 
-extern void note_launch();
-void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, const CUtensorMap& tm_vt,
-                         const CUtensorMap& tm_ut_half, const CUtensorMap& tm_h, const CUtensorMap& tm_o,
-                         ffn::Params p, int schedule, int* flags, const void* X, float* rstat, int* stats_ready,
-                         cudaStream_t stream);
+void ffn_swiglu_bf16_2sm(const Plan& pl, const void* X, const void* Wt, const void* Vt, const void* Ut, void* O,
+                         void* H, float* rstat, int* counters, float eps, cudaStream_t stream);
 
 void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
                      int64_t F, int64_t N, float eps, int schedule, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -372,7 +390,15 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   void* H = wsb;
   float* rstat = reinterpret_cast<float*>(wsb + ffn_h_bytes(M, F));
-  int* flags = reinterpret_cast<int*>(wsb + ffn_h_bytes(M, F) + ffn_rstat_bytes(M));
+  int* counters = reinterpret_cast<int*>(wsb + ffn_h_bytes(M, F) + ffn_rstat_bytes(M));
+  // counters: [flags ...][stats_ready][wave][seg], zeroed once per call
+  BF_CUDA(cudaMemsetAsync(counters, 0, ffn_flag_count(M) * sizeof(int), stream));
+
+  const Plan pl = plan_ffn(M, D, F, N, BF_DTYPE_BF16, schedule);
+  if (pl.spec.cluster == 2) {
+    ffn_swiglu_bf16_2sm(pl, X, Wt, Vt, Ut, O, H, rstat, counters, eps, stream);
+    return;
+  }
 
   const CUtensorMap tm_x = make_tmap_bf16(X, M, D, D, BK, BM);
   const CUtensorMap tm_wt = make_tmap_bf16(Wt, F, D, D, BK, BF);
@@ -386,85 +412,28 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
   p.D = static_cast<int>(D);
   p.F = static_cast<int>(F);
   p.N = static_cast<int>(N);
-  p.Mt = static_cast<int>((M + BM - 1) / BM);
+  p.Mt = static_cast<int>(pl.units);
   p.Ft = static_cast<int>((F + BF - 1) / BF);
   p.Nt = static_cast<int>((N + BN - 1) / BN);
   p.kt_d = static_cast<int>((D + BK - 1) / BK);
   p.kt_f = static_cast<int>((F + BK - 1) / BK);
   p.inv_d = 1.0f / static_cast<float>(D);
   p.eps = eps;
-  p.flags = flags;
-  p.wave = nullptr;
-  p.seg = nullptr;
-  p.seg_tiles = 0;
-  // Down-projection raster (BFGPU_FFN_BRASTER, m-units of 256 rows per block; 0 = off).
-  // CTA-pair default 8, measured at C3 (ncu DRAM read per launch; 2 s sustained TFLOP/s):
-  //   fused 1.99 GB (off) / 1.83 GB (8) / 2.06 GB (4); two-phase down launch 1.22 / 1.09 / 1.23;
-  //   sustained fused 1306 (off) vs 1313-1316 (8). scripts/exp_braster.sh
-  static const int braster_env = [] {
-    const char* v = std::getenv("BFGPU_FFN_BRASTER");
-    return v ? std::atoi(v) : -1;
-  }();
+  p.flags = counters;
+  p.group = pl.group;
   p.braster = 0;
-  // m-tiles per scheduling group: larger groups re-read the weights fewer times,
-  // smaller groups keep the live part of H small enough to stay in L2.
-  static const int group_env = [] {
-    const char* v = std::getenv("BFGPU_FFN_GROUP");
-    return v ? std::atoi(v) : 0;
-  }();
-  // Default: 32 m-tiles (4096 rows) per group, 16 (2048 rows) for launches of at least
-  // 1e13 FLOP, which run power-capped with the 2-SM kernel's wave sync on (same threshold,
-  // ffn_swiglu_2sm.cu). Measured (TFLOP/s, fused, 2-SM):
-  //   Llama-3-8B  (C3): g=16 1470, g=32 1581, g=64 1477 (1-SM: 1226 / 1304 / 1417 / 1251 at 8/16/32/64);
-  //     again with the final kernel, alternating: g=32 1542-1565, g=24 1509, g=16 1483-1493
-  //   Llama-3-70B (C5, power-capped), before the wave sync: g=16 941-964, g=32 1016,
-  //     g=64 1000-1024, g=128 983; with it, alternating runs: g=16 1267-1279, g=32 1212-1265,
-  //     g=8 1204, g=64 1122, g=128 1052 (scripts/exp_70b_group.sh)
-  // Smaller groups re-read the weights more often; larger ones let H and X thrash L2.
-  const double flops = 2.0 * static_cast<double>(M) * static_cast<double>(F) * (2.0 * D + N);
-  const int g2 = flops >= 1e13 ? 16 : 32;
-  p.group = group_env > 0 ? group_env : std::min(g2, p.Mt);
-
-  // CTA-pair path (default): 256-row m-units, B split across the pair.
-  static const bool force_1sm = [] {
-    const char* v = std::getenv("BFGPU_FFN_1SM");
-    return v && v[0] == '1';
-  }();
-  if (!force_1sm) {
-    Params q = p;
-    q.Mt = static_cast<int>((M + 2 * BM - 1) / (2 * BM));
-    q.group = std::max(1, p.group / 2);
-    q.braster = braster_env >= 0 ? braster_env : 8;
-    const CUtensorMap tm_ut_half = make_tmap_bf16(Ut, N, F, F, BK, 128);
-    ffn_swiglu_bf16_2sm(tm_x, tm_wt, tm_vt, tm_ut_half, tm_h, tm_o, q, schedule, flags, X, rstat,
-                        flags + q.Mt * 2, stream);
-    return;
-  }
-
-  const int dev = current_device();
-  const int sms = num_sms(dev);
-  static bool attr_set = false;
-  if (!attr_set) {
-    BF_CUDA(cudaFuncSetAttribute(ffn_swiglu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
-  }
 
   auto launch = [&](int mode) {
     Params q = p;
     q.mode = mode;
     const long long a_tiles = static_cast<long long>(q.Mt) * q.Ft;
     const long long b_tiles = static_cast<long long>(q.Mt) * q.Nt;
-    const long long tiles = mode == kFused ? a_tiles + b_tiles : (mode == kGateUpOnly ? a_tiles : b_tiles);
-    BF_CHECK_ARG(tiles < (1ll << 31), "bf_rms_ffn_swiglu: too many tiles");
-    q.num_tiles = static_cast<int>(tiles);
-    const int grid = static_cast<int>(std::min<long long>(tiles, sms));
-    ffn_swiglu_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_wt, tm_vt, tm_ut, tm_h, tm_o, q);
-    BF_CUDA(cudaGetLastError());
-    note_launch();
+    q.num_tiles = static_cast<int>(mode == kFused ? a_tiles + b_tiles : (mode == kGateUpOnly ? a_tiles : b_tiles));
+    Plan lp = pl;
+    lp.grid = std::min(pl.grid, q.num_tiles);
+    launch_planned(lp, ffn_swiglu_kernel, stream, tm_x, tm_wt, tm_vt, tm_ut, tm_h, tm_o, q);
   };
-
   if (schedule == BF_FFN_FUSED) {
-    BF_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(p.Mt) * 4, stream));
     launch(kFused);
   } else {
     launch(kGateUpOnly);

@@ -31,6 +31,7 @@
 #include "common.hpp"
 #include "ffn_common.cuh"
 #include "sm100.cuh"
+#include "plan.hpp"
 #include "tma_host.hpp"
 
 namespace bfgpu {
@@ -233,8 +234,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const __nv_bfloat16* rows[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) rows[k] = ex.X + static_cast<size_t>(min(r + k, r1 - 1)) * p.D;
-        float t1[4], t2[4];
-        warp_rows_moments_bf16<4>(rows, p.D, lane, t1, t2);
+        float t1[4], t2[4], piv[4];
+        warp_rows_moments_bf16<4>(rows, p.D, lane, t1, t2, piv);
         if (lane == 0)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -363,19 +364,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace ffn2
 
-extern void note_launch();
-
-// Launch the CTA-pair kernel. `flags` holds ceil(M/256)*2 ints, `stats` M floats + a counter.
-void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, const CUtensorMap& tm_vt,
-                         const CUtensorMap& tm_ut_half, const CUtensorMap& tm_h, const CUtensorMap& tm_o,
-                         ffn::Params p, int schedule, int* flags, const void* X, float* rstat, int* stats_ready,
-                         cudaStream_t stream) {
+KernelSpec ffn2_spec() {
   using namespace ffn2;
-  const int sms = num_sms(current_device());
-  static bool attr_set = false;
-  if (!attr_set) {
-    BF_CUDA(cudaFuncSetAttribute(ffn_swiglu_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
+  KernelSpec k;
+  k.name = "ffn_swiglu_2sm_kernel";
+  k.func = reinterpret_cast<const void*>(&ffn_swiglu_2sm_kernel);
+  k.threads = NUM_THREADS;
+  k.smem_bytes = SMEM_BYTES;
+  k.tmem_cols = TMEM_COLS;
+  k.cluster = 2;
+  k.tile_m = 2 * BM;
+  k.tile_n = BN;
+  k.tile_k = BK;
+  k.stages = STAGES;
+  k.grid_sync = true;  // row statistics, fused hand-off flags, wave/segment sync are grid-wide
+  return k;
+}
+
+// Launch the CTA-pair kernel as planned. `counters` = [2*Mt flags][stats_ready][wave][seg], zeroed.
+void ffn_swiglu_bf16_2sm(const Plan& pl, const void* X, const void* Wt, const void* Vt, const void* Ut, void* O,
+                         void* H, float* rstat, int* counters, float eps, cudaStream_t stream) {
+  using namespace ffn2;
+  const int64_t M = pl.dims[0], D = pl.dims[1], F = pl.dims[2], N = pl.dims[3];
+  const CUtensorMap tm_x = make_tmap_bf16(X, M, D, D, BK, BM);
+  const CUtensorMap tm_wt = make_tmap_bf16(Wt, F, D, D, BK, BF);
+  const CUtensorMap tm_vt = make_tmap_bf16(Vt, F, D, D, BK, BF);
+  const CUtensorMap tm_ut = make_tmap_bf16(Ut, N, F, F, BK, 128);
+  const CUtensorMap tm_h = make_tmap_bf16(H, M, F, F, BK, BM);
+  const CUtensorMap tm_o = make_tmap_bf16(O, M, N, N, BK, BM);
+
+  ffn::Params p{};
+  p.M = static_cast<int>(M);
+  p.D = static_cast<int>(D);
+  p.F = static_cast<int>(F);
+  p.N = static_cast<int>(N);
+  p.Mt = static_cast<int>(pl.units);
+  p.Ft = static_cast<int>((F + BF - 1) / BF);
+  p.Nt = static_cast<int>((N + BN - 1) / BN);
+  p.kt_d = static_cast<int>((D + BK - 1) / BK);
+  p.kt_f = static_cast<int>((F + BK - 1) / BK);
+  p.inv_d = 1.0f / static_cast<float>(D);
+  p.eps = eps;
+  p.flags = counters;
+  p.group = pl.group;
+  p.braster = pl.raster;
+  int* stats_ready = counters + 2 * p.Mt;
+  p.wave = pl.sync == kSyncWave ? stats_ready + 1 : nullptr;
+  p.seg = nullptr;
+  p.seg_tiles = 0;
+  if (pl.sync == kSyncSegment) {
+    // no cluster starts a tile past the first two gate/up segments before all of those started
+    const int ngroups = (p.Mt + p.group - 1) / p.group;
+    const int g0 = std::min(p.group, p.Mt), g1 = ngroups > 1 ? std::min(p.group, p.Mt - p.group) : 0;
+    p.seg = stats_ready + 2;
+    p.seg_tiles = (g0 + g1) * p.Ft;
   }
   Extra ex{static_cast<const __nv_bfloat16*>(X), rstat, stats_ready};
   auto launch = [&](int mode) {
@@ -383,45 +425,14 @@ void ffn_swiglu_bf16_2sm(const CUtensorMap& tm_x, const CUtensorMap& tm_wt, cons
     q.mode = mode;
     const long long a_tiles = static_cast<long long>(q.Mt) * q.Ft;
     const long long b_tiles = static_cast<long long>(q.Mt) * q.Nt;
-    const long long tiles = mode == kFused ? a_tiles + b_tiles : (mode == kGateUpOnly ? a_tiles : b_tiles);
-    BF_CHECK_ARG(tiles < (1ll << 31), "bf_rms_ffn_swiglu: too many tiles");
-    q.num_tiles = static_cast<int>(tiles);
-    const int clusters = static_cast<int>(std::min<long long>(tiles, sms / 2));
-    if (q.wave || q.seg) BF_CUDA(cudaMemsetAsync(stats_ready + 1, 0, 2 * sizeof(int), stream));
-    ffn_swiglu_2sm_kernel<<<clusters * 2, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_wt, tm_vt, tm_ut_half, tm_h,
-                                                                           tm_o, q, ex);
-    BF_CUDA(cudaGetLastError());
-    note_launch();
+    q.num_tiles = static_cast<int>(mode == kFused ? a_tiles + b_tiles : (mode == kGateUpOnly ? a_tiles : b_tiles));
+    Plan lp = pl;
+    lp.grid = std::min(pl.grid / 2, q.num_tiles) * 2;
+    // the wave counter restarts for every launch (the two-phase schedule launches twice)
+    if (q.wave && mode == kDownOnly) BF_CUDA(cudaMemsetAsync(q.wave, 0, sizeof(int), stream));
+    launch_planned(lp, ffn_swiglu_2sm_kernel, stream, tm_x, tm_wt, tm_vt, tm_ut, tm_h, tm_o, q, ex);
   };
-  // flags (fused hand-off) and the statistics counter live together: one memset
-  BF_CUDA(cudaMemsetAsync(flags, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
-  // Wave sync (BFGPU_FFN_WAVESYNC=1 forces it on, 0 off; default: on for launches of at
-  // least 1e13 FLOP, i.e. the ones long enough to run into the board power cap). Measured,
-  // Llama-3-70B (C5, 4.6e13 FLOP): fused 948 -> 1160 TFLOP/s (SM clock under the power cap
-  // 817 -> 1050 MHz), DRAM per two-phase step 80+47 -> 40+38 GB. Llama-3-8B (C3, 2.9e12
-  // FLOP, 1.9 ms, below the cap): DRAM 3.16 -> 2.65 GB but 1.5% slower (fused 1479-1578 vs
-  // 1555-1561, two-phase 1555-1559 vs 1580-1582, three A/B pairs on one box).
-  static const int wave_env = [] {
-    const char* v = std::getenv("BFGPU_FFN_WAVESYNC");
-    return v && v[0] ? (v[0] == '0' ? 0 : 1) : -1;
-  }();
-  const double flops = 2.0 * p.M * static_cast<double>(p.F) * (2.0 * p.D + p.N);
-  const bool wave_sync = wave_env >= 0 ? wave_env == 1 : flops >= 1e13;
-  p.wave = wave_sync ? stats_ready + 1 : nullptr;  // the spare int after the statistics counter
-  // Segment sync for the fused schedule when the wave sync is off (BFGPU_FFN_SEGSYNC=0 disables).
-  static const bool seg_env = [] {
-    const char* v = std::getenv("BFGPU_FFN_SEGSYNC");
-    return !(v && v[0] == '0');
-  }();
-  p.seg = nullptr;
-  p.seg_tiles = 0;
-  if (schedule == BF_FFN_FUSED && !wave_sync && seg_env) {
-    const int ngroups = (p.Mt + p.group - 1) / p.group;
-    const int g0 = std::min(p.group, p.Mt), g1 = ngroups > 1 ? std::min(p.group, p.Mt - p.group) : 0;
-    p.seg = stats_ready + 2;
-    p.seg_tiles = (g0 + g1) * p.Ft;
-  }
-  if (schedule == BF_FFN_FUSED) {
+  if (pl.schedule == BF_FFN_FUSED) {
     launch(kFused);
   } else {
     launch(kGateUpOnly);

@@ -28,6 +28,7 @@
 
 #include "common.hpp"
 #include "sm100.cuh"
+#include "plan.hpp"
 #include "tma_host.hpp"
 
 namespace bfgpu {
@@ -327,11 +328,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace lnmm
 
-extern void note_launch();
+KernelSpec lnmm1_spec() {
+  using namespace lnmm;
+  KernelSpec k;
+  k.name = "ln_matmul_kernel";
+  k.func = reinterpret_cast<const void*>(&ln_matmul_kernel);
+  k.threads = NUM_THREADS;
+  k.smem_bytes = SMEM_BYTES;
+  k.tmem_cols = TMEM_COLS;
+  k.cluster = 1;
+  k.tile_m = BM;
+  k.tile_n = BN;
+  k.tile_k = BK;
+  k.stages = STAGES;
+  k.grid_sync = true;  // colsum(Yt) published with a grid-wide counter
+  return k;
+}
 
 size_t lnmm2_workspace_bytes(int64_t M, int64_t N);
-void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
-                   size_t ws_bytes, cudaStream_t stream);
+void lnmm_bf16_2sm(const Plan& pl, const void* X, const void* Yt, void* O, float eps, void* ws, size_t ws_bytes,
+                   cudaStream_t stream);
 
 size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype) {
   (void)K;
@@ -347,13 +363,9 @@ void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int
   BF_CHECK_ARG(M < (1ll << 31) && K < (1ll << 31) && N < (1ll << 31), "bf_layernorm_matmul: dimension too large");
   BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm_workspace_bytes(M, K, N, BF_DTYPE_BF16),
                "bf_layernorm_matmul: workspace too small");
-  // CTA-pair kernel by default; BFGPU_LNMM_1SM=1 selects the 1-SM kernel below.
-  static const bool force_1sm = [] {
-    const char* v = std::getenv("BFGPU_LNMM_1SM");
-    return v && v[0] == '1';
-  }();
-  if (!force_1sm) {
-    lnmm_bf16_2sm(X, Yt, O, M, K, N, eps, ws, ws_bytes, stream);
+  const Plan pl = plan_lnmm(M, K, N, BF_DTYPE_BF16);
+  if (pl.spec.cluster == 2) {
+    lnmm_bf16_2sm(pl, X, Yt, O, eps, ws, ws_bytes, stream);
     return;
   }
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -368,30 +380,17 @@ void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int
   p.M = static_cast<int>(M);
   p.K = static_cast<int>(K);
   p.N = static_cast<int>(N);
-  p.Mt = static_cast<int>((M + BM - 1) / BM);
+  p.Mt = static_cast<int>(pl.units);
   p.Nt = static_cast<int>((N + BN - 1) / BN);
   p.kt = static_cast<int>((K + BK - 1) / BK);
-  p.group = 8;
+  p.group = pl.group;
   p.inv_k = 1.0f / static_cast<float>(K);
   p.eps = eps;
   p.colsum = colsum;
   p.ready = ready;
-  const long long tiles = static_cast<long long>(p.Mt) * p.Nt;
-  BF_CHECK_ARG(tiles < (1ll << 31), "bf_layernorm_matmul: too many tiles");
-  p.num_tiles = static_cast<int>(tiles);
-
-  const int sms = num_sms(current_device());
-  static bool attr_set = false;
-  if (!attr_set) {
-    BF_CUDA(cudaFuncSetAttribute(ln_matmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
-  }
-  const int grid = static_cast<int>(std::min<long long>(tiles, sms));
+  p.num_tiles = static_cast<int>(pl.tiles);
   BF_CUDA(cudaMemsetAsync(ready, 0, sizeof(int), stream));
-  ln_matmul_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_y, tm_o,
-                                                               static_cast<const __nv_bfloat16*>(Yt), p);
-  BF_CUDA(cudaGetLastError());
-  note_launch();
+  launch_planned(pl, ln_matmul_kernel, stream, tm_x, tm_y, tm_o, static_cast<const __nv_bfloat16*>(Yt), p);
 }
 
 }  // namespace bfgpu

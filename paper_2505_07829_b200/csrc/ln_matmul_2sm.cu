@@ -24,6 +24,7 @@
 
 #include "common.hpp"
 #include "sm100.cuh"
+#include "plan.hpp"
 #include "tma_host.hpp"
 
 namespace bfgpu {
@@ -194,11 +195,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     bool col_seen = false;
     const int num_rt = (p.M + BM - 1) / BM;
-    auto publish = [&](int r, float t1, float t2) {
-      const float mean = t1 * p.inv_k;
-      // var = t2/total(K) + (0 - square(t1/total(K)))  [+ eps, 0 in the reference]
-      p.row_mu[r] = -mean;
-      p.row_rstd[r] = 1.0f / sqrtf(t2 * p.inv_k - mean * mean + p.eps);
+    auto publish = [&](int r, float t1, float t2, float piv) {
+      // moments about the pivot: t1 = sum (x - piv), t2 = sum (x - piv)^2, so
+      // var = t2/total(K) + (0 - square(t1/total(K))) of the fused program [+ eps, 0 in the
+      // reference] is the same quantity without the cancellation of E[x^2] - mu^2
+      const float dm = t1 * p.inv_k;
+      p.row_mu[r] = -(piv + dm);
+      p.row_rstd[r] = 1.0f / sqrtf(t2 * p.inv_k - dm * dm + p.eps);
     };
     auto compute_row_tile = [&](int rt) {
       // kRows rows per warp at a time: these loads stream while the tensor cores run, and
@@ -211,12 +214,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const __nv_bfloat16* rows[kRows];
 #pragma unroll
         for (int k = 0; k < kRows; ++k) rows[k] = p.X + static_cast<size_t>(min(r0 + k, p.M - 1)) * p.K;
-        float t1[kRows], t2[kRows];
-        warp_rows_moments_bf16<kRows>(rows, p.K, lane, t1, t2);
+        float t1[kRows], t2[kRows], piv[kRows];
+        warp_rows_moments_bf16<kRows, true>(rows, p.K, lane, t1, t2, piv);
         if (lane == 0)
 #pragma unroll
           for (int k = 0; k < kRows; ++k)
-            if (r0 + k < p.M) publish(r0 + k, t1[k], t2[k]);
+            if (r0 + k < p.M) publish(r0 + k, t1[k], t2[k], piv[k]);
       }
       named_bar_sync(1, EPI_THREADS);
       if (store_leader) {
@@ -329,7 +332,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace lnmm2
 
-extern void note_launch();
+KernelSpec lnmm2_spec() {
+  using namespace lnmm2;
+  KernelSpec k;
+  k.name = "ln_matmul_2sm_kernel";
+  k.func = reinterpret_cast<const void*>(&ln_matmul_2sm_kernel);
+  k.threads = NUM_THREADS;
+  k.smem_bytes = SMEM_BYTES;
+  k.tmem_cols = TMEM_COLS;
+  k.cluster = 2;
+  k.tile_m = 2 * BM;
+  k.tile_n = BN;
+  k.tile_k = BK;
+  k.stages = STAGES;
+  k.grid_sync = true;  // colsum counter and per-row-tile statistics flags are grid-wide
+  return k;
+}
 
 size_t lnmm2_workspace_bytes(int64_t M, int64_t N) {
   const size_t mt = static_cast<size_t>((M + 255) / 256) * 2;
@@ -337,27 +355,20 @@ size_t lnmm2_workspace_bytes(int64_t M, int64_t N) {
          align_up((mt + 1) * 4, 256);
 }
 
-void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
-                   size_t ws_bytes, cudaStream_t stream) {
+void lnmm_bf16_2sm(const Plan& pl, const void* X, const void* Yt, void* O, float eps, void* ws, size_t ws_bytes,
+                   cudaStream_t stream) {
   using namespace lnmm2;
+  const int64_t M = pl.dims[0], K = pl.dims[1], N = pl.dims[2];
   BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm2_workspace_bytes(M, N), "bf_layernorm_matmul: workspace too small");
   uint8_t* w = static_cast<uint8_t*>(ws);
   Params p{};
   p.M = static_cast<int>(M);
   p.K = static_cast<int>(K);
   p.N = static_cast<int>(N);
-  p.Mt = static_cast<int>((M + 255) / 256);
+  p.Mt = static_cast<int>(pl.units);
   p.Nt = static_cast<int>((N + BN - 1) / BN);
   p.kt = static_cast<int>((K + BK - 1) / BK);
-  // m-units (256 rows) per scheduling group; n is the slow index inside a group, so the
-  // group's X rows (16 x 2 MB at K = 4096) stay in L2 while its n-tiles pass. Measured at
-  // C4 (scripts/exp_lnmm.sh): g = 2/4/8/16/32 -> 993/1382/1398/1481/1386 TFLOP/s, DRAM
-  // 1.39/1.41/1.88/1.89/3.23 GB per launch.
-  static const int group_env = [] {
-    const char* v = std::getenv("BFGPU_LNMM_GROUP");
-    return v ? std::atoi(v) : 0;
-  }();
-  p.group = group_env > 0 ? group_env : 16;
+  p.group = pl.group;
   p.inv_k = 1.0f / static_cast<float>(K);
   p.eps = eps;
   p.X = static_cast<const __nv_bfloat16*>(X);
@@ -370,24 +381,13 @@ void lnmm_bf16_2sm(const void* X, const void* Yt, void* O, int64_t M, int64_t K,
   w += align_up(static_cast<size_t>(M) * 4, 256);
   p.col_ready = reinterpret_cast<int*>(w);
   p.row_ready = p.col_ready + 1;
-  const long long tiles = static_cast<long long>(p.Mt) * p.Nt;
-  BF_CHECK_ARG(tiles < (1ll << 31), "bf_layernorm_matmul: too many tiles");
-  p.num_tiles = static_cast<int>(tiles);
+  p.num_tiles = static_cast<int>(pl.tiles);
 
   const CUtensorMap tm_x = make_tmap_bf16(X, M, K, K, BK, BM);
   const CUtensorMap tm_y = make_tmap_bf16(Yt, N, K, K, BK, 128);
   const CUtensorMap tm_o = make_tmap_bf16(O, M, N, N, BK, BM);
-  static bool attr_set = false;
-  if (!attr_set) {
-    BF_CUDA(cudaFuncSetAttribute(ln_matmul_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
-  }
-  const int sms = num_sms(current_device());
-  const int clusters = static_cast<int>(std::min<long long>(tiles, sms / 2));
   BF_CUDA(cudaMemsetAsync(p.col_ready, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
-  ln_matmul_2sm_kernel<<<clusters * 2, NUM_THREADS, SMEM_BYTES, stream>>>(tm_x, tm_y, tm_o, p);
-  BF_CUDA(cudaGetLastError());
-  note_launch();
+  launch_planned(pl, ln_matmul_2sm_kernel, stream, tm_x, tm_y, tm_o, p);
 }
 
 }  // namespace bfgpu

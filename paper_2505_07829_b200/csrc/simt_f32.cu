@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "common.hpp"
+#include "plan.hpp"
 
 namespace bfgpu {
 
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   __shared__ float B2s[EPI == kSwiGLU ? BK : 1][BN + 4];
-  __shared__ float row_s1[BM], row_s2[BM], col_s[BN];
+  __shared__ float row_s1[BM], row_s2[BM], row_piv[BM], col_s[BN];
 
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
@@ -47,12 +48,18 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   float acc[4][4] = {};
   float acc2[4][4] = {};
   float s1 = 0.f, s2 = 0.f, cs = 0.f;  // stats owned by threads < 64 (rows) and 64..127 (cols)
+  // K2 moments are taken about the row's first element (shifted moments: no E[x^2] - mu^2
+  // cancellation when |mean| >> sigma); K1 needs the plain sum of squares.
+  // For K2 the contraction runs on the shifted rows too: (X - p) Yt^T - (mu - p) colsum(Yt) is
+  // the same value as X Yt^T - mu colsum(Yt), without the fp32 cancellation of two large terms.
+  if (EPI == kLNMM && tid < BM) row_piv[tid] = m0 + tid < M ? A[static_cast<size_t>(m0 + tid) * K] : 0.f;
+  if constexpr (EPI == kLNMM) __syncthreads();
 
   for (int k0 = 0; k0 < K; k0 += BK) {
     for (int i = tid; i < BM * BK; i += THREADS) {
       const int r = i / BK, c = i % BK;
       const int gm = m0 + r, gk = k0 + c;
-      As[c][r] = (gm < M && gk < K) ? A[static_cast<size_t>(gm) * K + gk] : 0.f;
+      As[c][r] = (gm < M && gk < K) ? A[static_cast<size_t>(gm) * K + gk] - (EPI == kLNMM ? row_piv[r] : 0.f) : 0.f;
       const int gn = n0 + r;
       Bs[c][r] = (gn < N && gk < K) ? B[static_cast<size_t>(gn) * K + gk] : 0.f;
       if constexpr (EPI == kSwiGLU) B2s[c][r] = (gn < N && gk < K) ? B2[static_cast<size_t>(gn) * K + gk] : 0.f;
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
       if (tid < BM) {
 #pragma unroll
         for (int c = 0; c < BK; ++c) {
-          const float x = As[c][tid];
+          const float x = As[c][tid];  // zero past K (and already shifted for K2)
           s1 += x;
           s2 = fmaf(x, x, s2);
         }
@@ -106,9 +113,10 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     float scale = 1.f, mu = 0.f;
     if constexpr (EPI == kSwiGLU) scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k + ep.eps);
     if constexpr (EPI == kLNMM) {
-      mu = row_s1[r] * ep.inv_k;
-      // var = t2/total(K) + (0 - square(t1/total(K)))   (fused program)
-      scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k - mu * mu + ep.eps);
+      const float dm = row_s1[r] * ep.inv_k;
+      mu = dm;  // the accumulator holds (X - p) Yt^T: subtract (mu - p) colsum(Yt)
+      // var = t2/total(K) + (0 - square(t1/total(K)))   (fused program), moments about the pivot
+      scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k - dm * dm + ep.eps);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -222,6 +230,33 @@ void launch_gemm(const float* A, const float* B, const float* B2, float* C, int6
 }
 
 }  // namespace simt
+
+KernelSpec simt_gemm_spec(int epi) {
+  KernelSpec k;
+  k.name = epi == simt::kSwiGLU ? "gemm_f32_kernel<swiglu>" : (epi == simt::kLNMM ? "gemm_f32_kernel<lnmm>" : "gemm_f32_kernel");
+  k.func = epi == simt::kSwiGLU ? reinterpret_cast<const void*>(&simt::gemm_f32_kernel<simt::kSwiGLU>)
+           : epi == simt::kLNMM ? reinterpret_cast<const void*>(&simt::gemm_f32_kernel<simt::kLNMM>)
+                                : reinterpret_cast<const void*>(&simt::gemm_f32_kernel<simt::kPlain>);
+  k.threads = simt::THREADS;
+  k.tile_m = simt::BM;
+  k.tile_n = simt::BN;
+  k.tile_k = simt::BK;
+  k.stages = 1;
+  k.tensor = false;
+  return k;
+}
+
+KernelSpec simt_attn_spec() {
+  KernelSpec k;
+  k.name = "attn_f32_kernel";
+  k.func = reinterpret_cast<const void*>(&simt::attn_f32_kernel);
+  k.threads = simt::ATHREADS;
+  k.tile_m = simt::AQ;
+  k.tile_n = simt::AKV;
+  k.stages = 1;
+  k.tensor = false;
+  return k;
+}
 
 size_t ffn_f32_workspace_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 4, 256); }
 

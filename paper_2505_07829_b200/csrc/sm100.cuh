@@ -557,12 +557,22 @@ __device__ __forceinline__ float2 warp_row_moments_bf16(const __nv_bfloat16* row
 // R rows at once (8R independent 16-byte loads per lane in flight): sum x into s1[r] and
 // sum x^2 into s2[r] for row rows[r], in every lane. For statistics that must stream from
 // L2/HBM while the tensor cores run: R times the bytes in flight of the one-row version.
-template <int R>
+// With SHIFT, the moments are taken about a per-row pivot (the row's first element, returned in
+// piv[r]): s1 = sum (x - p), s2 = sum (x - p)^2. Then var = s2/n - (s1/n)^2 does not cancel
+// catastrophically when |mean| >> sigma (plain E[x^2] - E[x]^2 loses log2((mu/sigma)^2) bits).
+template <int R, bool SHIFT = false>
 __device__ __forceinline__ void warp_rows_moments_bf16(const __nv_bfloat16* const (&rows)[R], int n, uint32_t lane,
-                                                       float (&s1)[R], float (&s2)[R]) {
+                                                       float (&s1)[R], float (&s2)[R], float (&piv)[R]) {
   const int nv = n >> 3;
 #pragma unroll
-  for (int r = 0; r < R; ++r) s1[r] = s2[r] = 0.f;
+  uint32_t pad[R];  // what lanes past the row end contribute: the pivot itself (x - p = 0)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    s1[r] = s2[r] = 0.f;
+    const uint32_t b = SHIFT ? static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(rows[r]))) : 0u;
+    piv[r] = __uint_as_float(b << 16);
+    pad[r] = b | (b << 16);
+  }
   for (int c0 = 0; c0 < nv; c0 += 32 * 8) {
     uint4 v[R][8];
 #pragma unroll
@@ -570,7 +580,7 @@ __device__ __forceinline__ void warp_rows_moments_bf16(const __nv_bfloat16* cons
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int c = c0 + u * 32 + static_cast<int>(lane);
-        v[r][u] = c < nv ? __ldg(reinterpret_cast<const uint4*>(rows[r]) + c) : make_uint4(0u, 0u, 0u, 0u);
+        v[r][u] = c < nv ? __ldg(reinterpret_cast<const uint4*>(rows[r]) + c) : make_uint4(pad[r], pad[r], pad[r], pad[r]);
       }
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -579,7 +589,11 @@ __device__ __forceinline__ void warp_rows_moments_bf16(const __nv_bfloat16* cons
         const uint32_t w[4] = {v[r][u].x, v[r][u].y, v[r][u].z, v[r][u].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
+          float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
+          if (SHIFT) {
+            lo -= piv[r];
+            hi -= piv[r];
+          }
           s1[r] += lo + hi;
           s2[r] = fmaf(lo, lo, fmaf(hi, hi, s2[r]));
         }

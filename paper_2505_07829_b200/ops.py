@@ -9,7 +9,8 @@ from __future__ import annotations
 import torch
 
 from . import _lib
-from ._lib import BF_DTYPE_BF16, BF_DTYPE_F32, BF_FFN_FUSED, BF_FFN_TWO_PHASE, check
+from ._lib import (BF_DTYPE_BF16, BF_DTYPE_F32, BF_FFN_FUSED, BF_FFN_TWO_PHASE, BF_PATTERN_ATTENTION,
+                   BF_PATTERN_LAYERNORM_MATMUL, BF_PATTERN_RMS_FFN_SWIGLU, check)
 
 # one cached workspace per (device, stream): calls on different streams may overlap
 _WS: dict[tuple[int, int], torch.Tensor] = {}
@@ -74,13 +75,14 @@ def rms_ffn_swiglu(X, Wt, Vt, Ut, eps: float = 0.0, schedule: str = "fused", out
     code = _dtype_code(X)
     L = _lib.lib()
     nbytes = L.bf_rms_ffn_swiglu_workspace_bytes(M, D, F, N, code, sched)
-    ws = workspace if workspace is not None else _workspace(nbytes, dev)
-    check(
-        L.bf_rms_ffn_swiglu(
-            X.data_ptr(), Wt.data_ptr(), Vt.data_ptr(), Ut.data_ptr(), out.data_ptr(), M, D, F, N, code,
-            float(eps), sched, ws.data_ptr(), ws.numel(), _stream_ptr(dev),
+    with torch.cuda.device(dev):  # the C-ABI launches on the current device
+        ws = workspace if workspace is not None else _workspace(nbytes, dev)
+        check(
+            L.bf_rms_ffn_swiglu(
+                X.data_ptr(), Wt.data_ptr(), Vt.data_ptr(), Ut.data_ptr(), out.data_ptr(), M, D, F, N, code,
+                float(eps), sched, ws.data_ptr(), ws.numel(), _stream_ptr(dev),
+            )
         )
-    )
     return out
 
 
@@ -98,13 +100,14 @@ def layernorm_matmul(X, Yt, eps: float = 0.0, out=None, workspace=None):
     code = _dtype_code(X)
     L = _lib.lib()
     nbytes = L.bf_layernorm_matmul_workspace_bytes(M, K, N, code)
-    ws = workspace if workspace is not None else _workspace(nbytes, dev)
-    check(
-        L.bf_layernorm_matmul(
-            X.data_ptr(), Yt.data_ptr(), out.data_ptr(), M, K, N, code, float(eps), ws.data_ptr(), ws.numel(),
-            _stream_ptr(dev),
+    with torch.cuda.device(dev):
+        ws = workspace if workspace is not None else _workspace(nbytes, dev)
+        check(
+            L.bf_layernorm_matmul(
+                X.data_ptr(), Yt.data_ptr(), out.data_ptr(), M, K, N, code, float(eps), ws.data_ptr(), ws.numel(),
+                _stream_ptr(dev),
+            )
         )
-    )
     return out
 
 
@@ -128,17 +131,39 @@ def attention(Q, K, Vt, scale: float | None = None, out=None):
         out = torch.empty((*lead, Sq, Dv), dtype=dt, device=dev)
     _require(out, "out", (*lead, Sq, Dv), dt, dev)
     L = _lib.lib()
-    check(
-        L.bf_attention(
-            Q.data_ptr(), K.data_ptr(), Vt.data_ptr(), out.data_ptr(), BH, Sq, Skv, D, Dv, _dtype_code(Q),
-            float(scale) if scale is not None else 0.0, _stream_ptr(dev),
+    with torch.cuda.device(dev):
+        check(
+            L.bf_attention(
+                Q.data_ptr(), K.data_ptr(), Vt.data_ptr(), out.data_ptr(), BH, Sq, Skv, D, Dv, _dtype_code(Q),
+                float(scale) if scale is not None else 0.0, _stream_ptr(dev),
+            )
         )
-    )
     return out
 
 
 def kernel_launches() -> int:
     return int(_lib.lib().bf_kernel_launches())
+
+
+def plan(pattern: str, dims, dtype=torch.bfloat16, schedule: str = "fused", device=None) -> dict:
+    """The planner's launch plan (kernel, tiles, SMEM/TMEM budgets, grid, group, sync) for a call.
+
+    pattern: "rms_ffn_swiglu" (dims M, D, F, N), "layernorm_matmul" (M, K, N) or
+    "attention" (BH, Sq, Skv, D, Dv).
+    """
+    import ctypes
+    import json
+
+    pid = {"rms_ffn_swiglu": BF_PATTERN_RMS_FFN_SWIGLU, "layernorm_matmul": BF_PATTERN_LAYERNORM_MATMUL,
+           "attention": BF_PATTERN_ATTENTION}[pattern]
+    arr = (ctypes.c_int64 * len(dims))(*[int(d) for d in dims])
+    buf = ctypes.create_string_buffer(8192)
+    code = BF_DTYPE_BF16 if dtype == torch.bfloat16 else BF_DTYPE_F32
+    sched = {"fused": BF_FFN_FUSED, "two_phase": BF_FFN_TWO_PHASE}[schedule]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        check(_lib.lib().bf_plan_json(pid, arr, len(dims), code, sched, buf, len(buf)))
+    return json.loads(buf.value.decode())
 
 
 # ----------------------------------------------------------------- host-buffer calls
@@ -166,8 +191,11 @@ def _side_stream(device: torch.device, name: str) -> torch.cuda.Stream:
     return s
 
 
-def _device_like(t: torch.Tensor, device: torch.device, tag: str) -> torch.Tensor:
-    key = (device.index, tag, tuple(t.shape), t.dtype)
+def _device_like(t: torch.Tensor, device: torch.device, tag: tuple) -> torch.Tensor:
+    # keyed by the call signature and slot, never by shape alone: buffers are reused only by
+    # calls whose slot events order them (two signatures with a same-shaped operand must not
+    # share a buffer, or one call's H2D could overwrite it while the other's kernels read it)
+    key = (device.index, tag)
     b = _HOST_BUFS.get(key)
     if b is None:
         b = torch.empty(t.shape, dtype=t.dtype, device=device)
@@ -196,9 +224,9 @@ def from_host(fn, row_inputs, shared_inputs, out_host, chunks: int = 4, **kwargs
     state = _SLOTS.setdefault(sig, {"next": 0, "computed": [None, None]})
     slot = state["next"]
     state["next"] ^= 1
-    row_dev = [_device_like(t, dev, f"row{i}/{slot}") for i, t in enumerate(row_inputs)]
-    shared_dev = [_device_like(t, dev, f"shared{i}/{slot}") for i, t in enumerate(shared_inputs)]
-    out_dev = _device_like(out_host, dev, f"out/{slot}")
+    row_dev = [_device_like(t, dev, (sig, "row", i, slot)) for i, t in enumerate(row_inputs)]
+    shared_dev = [_device_like(t, dev, (sig, "shared", i, slot)) for i, t in enumerate(shared_inputs)]
+    out_dev = _device_like(out_host, dev, (sig, "out", 0, slot))
     if state["computed"][slot] is not None:
         h2d.wait_event(state["computed"][slot])  # kernels of the last call on this slot are done
     else:

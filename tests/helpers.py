@@ -68,3 +68,55 @@ def assert_f32_close(out, ref, what: str = "") -> None:
     assert np.all(np.isfinite(out)), f"{what}: non-finite output"
     r = rel_err(out, ref)
     assert r <= F32_REL_TOL, f"{what}: max|d|/max|ref| = {r:.3e} > {F32_REL_TOL}"
+
+
+class DeviceErr:
+    """The parity metrics above, accumulated on the GPU over chunks of a large output.
+
+    Full-shape outputs (C2-C5) are compared element by element against a torch fp32
+    reference computed on the device from the same bf16 inputs (TF32 off), without
+    moving the output to the host: max|d|/max|ref| and the rms-normalized allclose
+    excess max(|d| - rtol |ref|)/rms - atol."""
+
+    def __init__(self, rtol: float = BF16_REL_TOL):
+        self.rtol = rtol
+        self.max_d = 0.0
+        self.max_ref = 0.0
+        self.max_dr = -float("inf")
+        self.sq = 0.0
+        self.n = 0
+        self.nonfinite = 0
+
+    def add(self, out, ref) -> None:
+        import torch
+
+        o = out.float()
+        r = ref.float()
+        d = (o - r).abs()
+        self.nonfinite += int((~torch.isfinite(o)).sum().item())
+        self.max_d = max(self.max_d, float(d.max().item()))
+        self.max_ref = max(self.max_ref, float(r.abs().max().item()))
+        self.max_dr = max(self.max_dr, float((d - self.rtol * r.abs()).max().item()))
+        self.sq += float(r.double().pow(2).sum().item())
+        self.n += r.numel()
+
+    def summary(self) -> dict:
+        rms = (self.sq / max(self.n, 1)) ** 0.5
+        return {"rel": self.max_d / max(self.max_ref, 1e-300), "norm_abs": self.max_d / max(rms, 1e-300),
+                "excess": self.max_dr / max(rms, 1e-300), "nonfinite": self.nonfinite, "elements": self.n}
+
+    def check(self, what: str, norm_tol: float = BF16_NORM_ABS_TOL) -> dict:
+        s = self.summary()
+        print(f"{what}: {s}")
+        assert s["nonfinite"] == 0, f"{what}: {s['nonfinite']} non-finite outputs"
+        assert s["rel"] <= BF16_REL_TOL, f"{what}: max|d|/max|ref| = {s['rel']:.3e} > {BF16_REL_TOL}"
+        assert s["excess"] - norm_tol <= 0, f"{what}: normalized |d| exceeds {norm_tol} + 2e-2|ref| ({s})"
+        return s
+
+
+def stratified_rows(M: int, unit: int, seed: int = 0) -> np.ndarray:
+    """One row in every `unit`-row m-unit (the last, possibly ragged, unit included), at a
+    random offset: every m-unit, scheduling group and raster block of a launch is hit."""
+    rng = np.random.default_rng(seed)
+    starts = np.arange(0, M, unit)
+    return np.array([s + rng.integers(0, min(unit, M - s)) for s in starts], dtype=np.int64)
