@@ -9,7 +9,11 @@ runs shard token rows across ranks (weak scaling: every rank owns 8192 tokens),
 with no collective on the data path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload ffn_8b|ffn_70b|lnmm|attn] [--schedule fused|two_phase]
+                    [--workload ffn_8b|ffn_70b|lnmm|lnmm_c1|attn] [--schedule fused|two_phase]
+                    [--rows R]  (per-rank rows/heads override: e.g. the 8-GPU shard size on one GPU)
+
+Workloads are BASELINE.json's configs: C1 lnmm_c1 (LN->MM 1024^3 fp32), C2 attn,
+C3 ffn_8b (headline), C4 lnmm, C5 ffn_70b.
 
 `--impl reference` times the reference's own CPU executor (blockfuse::execute on
 the final fused snapshot, compiled in place from /root/reference into
@@ -19,7 +23,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -34,21 +37,29 @@ from paper_2505_07829_b200.launcher import max_over_ranks, shard  # noqa: E402
 
 METRIC = "fused RMSNorm+SwiGLU-FFN TFLOP/s & % bf16 peak; HBM bytes vs unfused"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# FP32 FMA peak (C1's roofline): 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz, unless measured
+# by scripts/micro/ffma_peak.cu into profiles/fp32_peak.json.
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 WORKLOADS = {
     # C3 (the headline): 8192 tokens per rank (weak scaling).
-    "ffn_8b": dict(kind="ffn", rows_per_rank=8192, D=4096, F=14336, N=4096, scaling="weak",
+    "ffn_8b": dict(kind="ffn", rows_per_rank=8192, D=4096, F=14336, N=4096, scaling="weak", dtype="bf16",
                    name="C3 RMSNorm->FFN-SwiGLU Llama-3-8B (d=4096, ffn=14336), 8192 tokens/GPU"),
     # C5: 32768 tokens row-sharded over the ranks (strong scaling).
-    "ffn_70b": dict(kind="ffn", rows_total=32768, D=8192, F=28672, N=8192, scaling="strong",
+    "ffn_70b": dict(kind="ffn", rows_total=32768, D=8192, F=28672, N=8192, scaling="strong", dtype="bf16",
                     name="C5 RMSNorm->FFN-SwiGLU Llama-3-70B (d=8192, ffn=28672), 32768 tokens row-sharded"),
     # C4: LayerNorm->MatMul M=65536 K=N=4096 row-sharded.
-    "lnmm": dict(kind="lnmm", rows_total=65536, K=4096, N=4096, scaling="strong",
-                 name="C4 LayerNorm->MatMul M=65536 K=N=4096, rows sharded"),
+    "lnmm": dict(kind="lnmm", rows_total=65536, K=4096, N=4096, scaling="strong", dtype="bf16",
+                 name="C4 LayerNorm->MatMul M=65536 K=N=4096 bf16, rows sharded"),
+    # C1: LayerNorm->MatMul M=K=N=1024 fp32 (the reference's CPU-runnable config).
+    "lnmm_c1": dict(kind="lnmm", rows_total=1024, K=1024, N=1024, scaling="strong", dtype="f32",
+                    name="C1 LayerNorm->MatMul M=K=N=1024 fp32"),
     # C2: FlashAttention B=8 H=32 S=2048 D=128, heads sharded.
-    "attn": dict(kind="attn", B=8, H=32, S=2048, Dh=128, scaling="strong",
+    "attn": dict(kind="attn", B=8, H=32, S=2048, Dh=128, scaling="strong", dtype="bf16",
                  name="C2 FlashAttention B=8 H=32 S=2048 D=128 non-causal, heads sharded"),
 }
+
+KERNELS = {"ffn": "ffn_swiglu_2sm_kernel", "lnmm": "ln_matmul_2sm_kernel", "attn": "attn_kernel"}
 
 
 # --------------------------------------------------------------------------- utils
@@ -60,6 +71,15 @@ def load_peaks() -> tuple[dict, str]:
         except Exception:
             pass
     return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+def fp32_peak() -> tuple[float, str]:
+    p = ROOT / "profiles" / "fp32_peak.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["tflops"]), f"measured ({d.get('how', 'scripts/micro/ffma_peak.cu')}, profiles/fp32_peak.json)"
+    except Exception:
+        return NOMINAL_FP32_TFLOPS, "nominal 148 SMs x 128 lanes x 2 x 1.965 GHz"
 
 
 def dist_info():
@@ -136,13 +156,13 @@ class ClockSampler:
                 "power_w_max": max(self.power_w) if self.power_w else None, "power_limit_w": self.power_limit_w}
 
 
-def unfused_measured(kind: str):
+def unfused_measured(wl_key: str):
     """DRAM bytes of one step of the unfused operator sequence (torch/cuBLAS kernels, one per
     top-level operator), measured with ncu by scripts/unfused_baseline.py (or None)."""
     p = ROOT / "profiles" / "unfused_baseline.json"
-    key = {"ffn": "ffn_8b", "lnmm": "lnmm", "attn": "attn"}[kind]
+    key = {"ffn_8b": "ffn_8b", "lnmm": "lnmm", "attn": "attn"}.get(wl_key)
     try:
-        return json.loads(p.read_text()).get(key)
+        return json.loads(p.read_text()).get(key) if key else None
     except Exception:
         return None
 
@@ -177,40 +197,48 @@ def ffn_bytes(M, D, F, N, eb=2):
     return fused, unfused
 
 
-def make_inputs(wl: dict, rank: int, world: int, device):
+def rows_for(wl: dict, rank: int, world: int, override: int | None) -> int:
+    if override:
+        return override
+    if wl["kind"] == "attn":
+        return shard(wl["B"] * wl["H"], rank, world).size
+    return wl.get("rows_per_rank") or shard(wl["rows_total"], rank, world, 128).size
+
+
+def make_inputs(wl: dict, rank: int, world: int, device, rows_override: int | None = None):
     import torch
 
     g = torch.Generator(device=device)
     kind = wl["kind"]
+    dt = torch.float32 if wl["dtype"] == "f32" else torch.bfloat16
+    eb = 4 if wl["dtype"] == "f32" else 2
+    rows = rows_for(wl, rank, world, rows_override)
     if kind == "ffn":
-        rows = wl.get("rows_per_rank") or shard(wl["rows_total"], rank, world, 128).size
         D, F, N = wl["D"], wl["F"], wl["N"]
         g.manual_seed(1234)  # weights identical on every rank (no broadcast needed)
-        Wt = (torch.randn(F, D, device=device, generator=g) * D ** -0.5).bfloat16()
-        Vt = (torch.randn(F, D, device=device, generator=g) * D ** -0.5).bfloat16()
-        Ut = (torch.randn(N, F, device=device, generator=g) * F ** -0.5).bfloat16()
+        Wt = (torch.randn(F, D, device=device, generator=g) * D ** -0.5).to(dt)
+        Vt = (torch.randn(F, D, device=device, generator=g) * D ** -0.5).to(dt)
+        Ut = (torch.randn(N, F, device=device, generator=g) * F ** -0.5).to(dt)
         g.manual_seed(1000 + rank)
-        X = torch.randn(rows, D, device=device, generator=g).bfloat16()
-        flops = 6.0 * rows * D * F
-        fused, unfused = ffn_bytes(rows, D, F, N)
-        return dict(X=X, Wt=Wt, Vt=Vt, Ut=Ut, rows=rows, flops=flops, fused_bytes=fused, unfused_bytes=unfused)
+        X = torch.randn(rows, D, device=device, generator=g).to(dt)
+        fused, unfused = ffn_bytes(rows, D, F, N, eb)
+        return dict(X=X, Wt=Wt, Vt=Vt, Ut=Ut, rows=rows, flops=6.0 * rows * D * F, fused_bytes=fused,
+                    unfused_bytes=unfused)
     if kind == "lnmm":
-        rows = shard(wl["rows_total"], rank, world, 128).size
         K, N = wl["K"], wl["N"]
         g.manual_seed(1234)
-        Yt = torch.randn(N, K, device=device, generator=g).bfloat16()
+        Yt = torch.randn(N, K, device=device, generator=g).to(dt)
         g.manual_seed(2000 + rank)
-        X = torch.randn(rows, K, device=device, generator=g).bfloat16()
-        return dict(X=X, Yt=Yt, rows=rows, flops=2.0 * rows * K * N, fused_bytes=2 * (rows * K + N * K + rows * N),
-                    unfused_bytes=2 * (rows * K * 2 + rows * K + N * K + rows * N))
-    B, H, S, Dh = wl["B"], wl["H"], wl["S"], wl["Dh"]
-    heads = shard(B * H, rank, world).size
+        X = torch.randn(rows, K, device=device, generator=g).to(dt)
+        return dict(X=X, Yt=Yt, rows=rows, flops=2.0 * rows * K * N, fused_bytes=eb * (rows * K + N * K + rows * N),
+                    unfused_bytes=eb * (rows * K * 2 + rows * K + N * K + rows * N))
+    S, Dh = wl["S"], wl["Dh"]
     g.manual_seed(3000 + rank)
-    Q = torch.randn(heads, S, Dh, device=device, generator=g).bfloat16()
-    K = torch.randn(heads, S, Dh, device=device, generator=g).bfloat16()
-    Vt = torch.randn(heads, Dh, S, device=device, generator=g).bfloat16()
-    return dict(Q=Q, K=K, Vt=Vt, rows=heads, flops=4.0 * heads * S * S * Dh,
-                fused_bytes=2 * 4 * heads * S * Dh, unfused_bytes=2 * heads * (4 * S * Dh + 3 * S * S))
+    Q = torch.randn(rows, S, Dh, device=device, generator=g).to(dt)
+    K = torch.randn(rows, S, Dh, device=device, generator=g).to(dt)
+    Vt = torch.randn(rows, Dh, S, device=device, generator=g).to(dt)
+    return dict(Q=Q, K=K, Vt=Vt, rows=rows, flops=4.0 * rows * S * S * Dh,
+                fused_bytes=eb * 4 * rows * S * Dh, unfused_bytes=eb * rows * (4 * S * Dh + 3 * S * S))
 
 
 def sum_over_ranks(value: float, device) -> float:
@@ -237,7 +265,7 @@ def step_fn(wl, inp, schedule, out):
 
 def check_output(wl, inp, out) -> dict:
     """Validate the timed output: stratified rows (one per 256-row m-unit) or heads against an
-    fp32 torch reference on the device, same bf16 inputs, TF32 off (tests/torch_ref.py)."""
+    fp32 torch reference on the device, same inputs, TF32 off (tests/torch_ref.py)."""
     import torch
 
     sys.path.insert(0, str(ROOT / "tests"))
@@ -246,6 +274,7 @@ def check_output(wl, inp, out) -> dict:
 
     kind = wl["kind"]
     err = DeviceErr()
+    f32 = wl["dtype"] == "f32"
     if kind in ("ffn", "lnmm"):
         rows = torch.arange(0, inp["rows"], 256, device=out.device)
         rows = torch.clamp(rows + torch.randint(0, 256, rows.shape, device=out.device, generator=torch.Generator(
@@ -265,88 +294,114 @@ def check_output(wl, inp, out) -> dict:
         what = f"{heads.numel()} heads of {inp['rows']}"
         tol = 2e-2
     s = err.summary()
-    s["pass"] = bool(s["nonfinite"] == 0 and s["rel"] <= 2e-2 and s["excess"] <= tol)
-    s["sample"] = what + ", vs fp32 torch reference on the same bf16 inputs"
+    rel_bar = 1e-4 if f32 else 2e-2
+    s["pass"] = bool(s["nonfinite"] == 0 and s["rel"] <= rel_bar and (f32 or s["excess"] <= tol))
+    s["sample"] = what + f", vs fp32 torch reference on the same {wl['dtype']} inputs (bar: max|d|/max|ref| <= {rel_bar:g})"
     return s
 
 
 # ------------------------------------------------------------------ CPU reference
-def reference_session(wl: dict, inp_shapes: dict, threads: int | None = None, shard_rows: int | None = None):
-    """Build a row-sharded reference-executor session for the workload (rank 0, host)."""
+def reference_session(wl: dict, threads: int | None = None, shard_rows: int | None = None):
+    """A row-sharded reference-executor session for the workload (rank 0, host):
+    blockfuse::execute on the final fused snapshot, one shard per worker thread."""
     import numpy as np
 
     from oracle import refexec as R
 
     cores = os.cpu_count() or 1
+    rng = np.random.default_rng(1234)
     if wl["kind"] == "ffn":
         D, F, N = wl["D"], wl["F"], wl["N"]
-        weight_bytes = 8 * (2 * F * D + N * F)
-        per_worker = 10 * weight_bytes  # input map + split grid + per-iteration broadcast copies
-        which, shared_names = R.RMS_FFN_SWIGLU, ("Wt", "Vt", "Ut")
+        per_worker = 10 * 8 * (2 * F * D + N * F)  # input map + split grid + per-iteration broadcast copies
+        which, row_name = R.RMS_FFN_SWIGLU, "X"
         rows = shard_rows or 128
         binding = {"M": (1, rows), "D": (D // 128, 128), "K": (F // 128, 128), "N": (1, N)}
+        bdesc = f"M=1x{rows} D={D // 128}x128 K={F // 128}x128 N=1x{N}"
         row_cols, out_cols = D, N
         flops_per_row = 6.0 * D * F
-        rng = np.random.default_rng(1234)
         shared = {"Wt": rng.standard_normal((F, D)) * D ** -0.5, "Vt": rng.standard_normal((F, D)) * D ** -0.5,
                   "Ut": rng.standard_normal((N, F)) * F ** -0.5}
-        row_name = "X"
+        unit = "row"
     elif wl["kind"] == "lnmm":
         K, N = wl["K"], wl["N"]
         per_worker = 10 * 8 * N * K
         which, row_name = R.LAYERNORM_MATMUL, "X"
         rows = shard_rows or 128
-        binding = {"M": (1, rows), "K": (K // 128, 128), "N": (N // 256, 256)}
+        nb = 256 if N % 256 == 0 and N >= 2048 else 128
+        binding = {"M": (rows // 128 if rows % 128 == 0 else 1, 128 if rows % 128 == 0 else rows),
+                   "K": (K // 128, 128), "N": (N // nb, nb)}
+        bdesc = f"M={binding['M'][0]}x{binding['M'][1]} K={K // 128}x128 N={N // nb}x{nb}"
         row_cols, out_cols = K, N
         flops_per_row = 2.0 * K * N
-        rng = np.random.default_rng(1234)
         shared = {"Yt": rng.standard_normal((N, K))}
+        unit = "row"
     else:
-        raise ValueError("reference sessions cover the row-sharded programs (ffn, lnmm)")
+        S, Dh = wl["S"], wl["Dh"]
+        per_worker = 64 * S * Dh * 8 + 40 * S * S * 8
+        which, row_name = R.ATTENTION, "Q"
+        rows = S  # one head's queries per worker
+        binding = {"M": (S // 128, 128), "N": (S // 128, 128), "D": (1, Dh), "L": (1, Dh)}
+        bdesc = f"M={S // 128}x128 N={S // 128}x128 D=1x{Dh} L=1x{Dh}"
+        row_cols, out_cols = Dh, Dh
+        flops_per_row = 4.0 * S * Dh
+        # the values of K and V do not change the executor's work; one head's K/Vt serve every
+        # worker's head (each worker has its own Q)
+        shared = {"K": rng.standard_normal((S, Dh)), "Vt": rng.standard_normal((Dh, S))}
+        unit = "head"
     try:
         avail = int(next(l for l in open("/proc/meminfo") if l.startswith("MemAvailable")).split()[1]) * 1024
     except Exception:
         avail = 32 << 30
     mem_workers = max(1, int((avail - (16 << 30)) // per_worker))
     workers = max(1, min(threads or cores, mem_workers))
+    if wl.get("rows_total") and wl["kind"] != "attn":
+        workers = min(workers, max(1, wl["rows_total"] // rows))  # never more than the whole problem
     sess = R.Session(which, R.FINAL, shared, row_name, row_cols, out_cols, binding, rows, workers)
-    rng = np.random.default_rng(7)
-    X = rng.standard_normal((workers * rows, row_cols))
-    return sess, X, workers, rows, flops_per_row
+    X = np.random.default_rng(7).standard_normal((workers * rows, row_cols))
+    return dict(sess=sess, X=X, workers=workers, rows=rows, flops_per_row=flops_per_row, binding=bdesc, unit=unit)
 
 
-def cpu_baseline(wl: dict, budget_s: float = 25.0) -> dict:
-    """Reference executor on a bounded sample (one 128-row block per host thread)."""
-    if wl["kind"] not in ("ffn", "lnmm"):
-        return None
-    t0 = time.time()
-    sess, X, workers, rows, fpr = reference_session(wl, {})
-    sess.step(X)  # warm-up (first call pays page faults for the block copies)
+def _time_session(s: dict, warmup: int, steps: int, budget_s: float) -> tuple[float, int]:
+    for _ in range(warmup):
+        s["sess"].step(s["X"])  # the first call pays page faults for the block copies
     t1 = time.time()
     n = 0
     while True:
-        sess.step(X)
+        s["sess"].step(s["X"])
         n += 1
-        if time.time() - t1 > budget_s / 3 or n >= 3:
+        if time.time() - t1 > budget_s or n >= steps:
             break
-    dt = (time.time() - t1) / n
-    sess.close()
-    # (i) the reference exactly as written: one thread, one 128-row shard (SURVEY.md §8(d))
+    return (time.time() - t1) / n, n
+
+
+def cpu_baseline(wl: dict, budget_s: float = 25.0) -> dict:
+    """Reference executor on a bounded sample: one shard (128 rows, or one head) per host thread,
+    plus the reference exactly as written (one thread)."""
+    t0 = time.time()
+    s = reference_session(wl)
+    dt, n = _time_session(s, 1, 3, budget_s / 3)
+    s["sess"].close()
+    work = s["flops_per_row"] * s["workers"] * s["rows"]
     single = None
     try:
-        s1, X1, w1, r1, _ = reference_session(wl, {}, threads=1)
-        s1.step(X1)  # warm-up
-        ts = time.time()
-        s1.step(X1)
-        d1 = time.time() - ts
-        s1.close()
-        single = {"value": fpr * w1 * r1 / d1 / 1e12, "unit": "TFLOP/s", "cores": 1, "seconds_per_step": d1,
-                  "sample": f"one {r1}-row shard, 1 thread, 1 step after 1 warm-up"}
+        # (i) the reference as written: one thread; C1 at full size, otherwise one shard
+        full = wl["kind"] == "lnmm" and wl.get("rows_total", 0) <= 1024
+        s1 = reference_session(wl, threads=1, shard_rows=wl["rows_total"] if full else None)
+        d1, _ = _time_session(s1, 1, 1, 0)
+        s1["sess"].close()
+        single = {"value": s1["flops_per_row"] * s1["rows"] / d1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                  "seconds_per_step": d1,
+                  "sample": (f"the whole problem ({s1['rows']} rows), 1 thread" if full else
+                             f"one {s1['rows']}-{s1['unit']} shard" if s1["unit"] == "row" else "one head") +
+                            f", binding {s1['binding']}, 1 step after 1 warm-up"}
     except Exception as e:  # noqa: BLE001 - reported, not fatal
         single = {"unavailable": str(e)}
-    return {"value": fpr * workers * rows / dt / 1e12, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
-            "sample": (f"blockfuse::execute on the final fused snapshot, {workers} concurrent row shards x {rows} rows "
-                       f"(one M block each), mean of {n} steps after 1 warm-up; setup+run {time.time() - t0:.0f} s"),
+    shard_desc = f"{s['rows']} rows" if s["unit"] == "row" else "one head (2048 queries)"
+    return {"value": work / dt / 1e12, "unit": "TFLOP/s", "cores": s["workers"], "kind": "reference",
+            "sample": (f"blockfuse::execute on the final fused snapshot, {s['workers']} concurrent shards of "
+                       f"{shard_desc} (binding {s['binding']}), mean of {n} steps after 1 warm-up; "
+                       f"setup+run {time.time() - t0:.0f} s; Eigen = the repo's Eigen-API stand-in "
+                       "(third_party/eigen_shim, packed AVX2 GEMM)"),
             "seconds_per_step": dt, "single_thread": single}
 
 
@@ -354,31 +409,104 @@ def run_reference_arm(args, wl):
     rank, world, _ = dist_info()
     if rank != 0:
         return 0
-    sess, X, workers, rows, fpr = reference_session(wl, {})
+    s = reference_session(wl)
     for _ in range(args.warmup):
-        sess.step(X)
+        s["sess"].step(s["X"])
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        sess.step(X)
+        s["sess"].step(s["X"])
         times.append(time.perf_counter() - t)
-    sess.close()
+    s["sess"].close()
     ms = 1e3 * sum(times) / len(times)
-    value = fpr * workers * rows / (ms / 1e3) / 1e12
+    value = s["flops_per_row"] * s["workers"] * s["rows"] / (ms / 1e3) / 1e12
+    shard_desc = f"{s['rows']}-row shards" if s["unit"] == "row" else "one head each"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,1) activations, N(0,1)/sqrt(fan_in) weights",
-        "config": {"workload": wl["name"], "sample_rows_per_step": workers * rows, "shard_rows": rows,
-                   "binding": "M=1x128 D=32x128 K=112x128 N=1x4096" if wl["kind"] == "ffn" else "M=1x128 K=32x128 N=16x256"},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
-                         "sample": f"{workers} threads x {rows}-row shards per step, blockfuse::execute (final snapshot), "
-                                   "reference headers compiled in place against the repo's Eigen-API shim"},
+        "config": {"workload": wl["name"], "sample_per_step": f"{s['workers']} x {shard_desc}",
+                   "binding": s["binding"]},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": s["workers"], "kind": "reference",
+                         "sample": f"{s['workers']} threads x {shard_desc} per step, blockfuse::execute (final "
+                                   "snapshot), reference headers compiled in place against the repo's Eigen-API "
+                                   "stand-in"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def reference_model(wl: dict, rows: int) -> dict:
+    """The reference's own traffic_bytes model (metrics.hpp:154-191) for this workload."""
+    try:
+        from oracle import refexec as R
+
+        if not R.available():
+            return {"error": "oracle/_ref/libbfref.so not built"}
+        eb = 4 if wl["dtype"] == "f32" else 2
+        if wl["kind"] == "ffn":
+            b = {"M": (rows // 128, 128), "N": (1, wl["N"]), "K": (1, wl["F"]), "D": (1, wl["D"])}
+            which, scale = R.RMS_FFN_SWIGLU, 1
+        elif wl["kind"] == "lnmm":
+            b = {"M": (rows // 128, 128), "K": (1, wl["K"]), "N": (1, wl["N"])}
+            which, scale = R.LAYERNORM_MATMUL, 1
+        else:
+            S, Dh = wl["S"], wl["Dh"]
+            b = {"M": (S // 128, 128), "N": (1, S), "D": (1, Dh), "L": (1, Dh)}
+            which, scale = R.ATTENTION, rows  # per head, times the heads
+        return {"binding": "M in 128-row blocks, contraction dims one block (counts=1)"
+                + (f", per head x {rows} heads" if wl["kind"] == "attn" else ""),
+                "element_bytes": eb,
+                "fused_final_snapshot": scale * R.traffic_bytes(which, R.FINAL, b, eb),
+                "unfused_lowered": scale * R.traffic_bytes(which, R.UNFUSED, b, eb)}
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
+def e2e_adapter(wl: dict, rows: int, precision: str, schedule: str) -> dict:
+    """End to end through the reference-facing C++ drop-in: `bfgpu::execute(program,
+    map<string, MatrixXd>, binding)` (host/bfgpu_execute.hpp, the signature of
+    blockfuse::execute, interpreter.hpp:478) on the fusion driver's final snapshot, timed by
+    bfgpu-cli run: float64 column-major inputs converted on the host threads into pinned
+    memory, uploaded, the kernel, the download and the widening back to float64, every call."""
+    import subprocess
+    import tempfile
+
+    cli = ROOT / "paper_2505_07829_b200" / "lib" / "bfgpu-cli"
+    if not cli.exists():
+        return {"unavailable": "bfgpu-cli not built"}
+    kind = wl["kind"]
+    ex = {"ffn": "rms-swiglu", "lnmm": "layernorm-matmul", "attn": "attention"}[kind]
+    if kind == "ffn":
+        dims = f"M={rows // 128},D={wl['D'] // 128},K={wl['F'] // 128},N={wl['N'] // 128}"
+        flops, what = 6.0 * rows * wl["D"] * wl["F"], f"{rows} rows"
+    elif kind == "lnmm":
+        dims = f"M={rows // 128},K={wl['K'] // 128},N={wl['N'] // 128}"
+        flops, what = 2.0 * rows * wl["K"] * wl["N"], f"{rows} rows"
+    else:
+        S, Dh = wl["S"], wl["Dh"]
+        dims = f"M={S // 128},N={S // 128},D={Dh // 128},L={Dh // 128}"
+        flops, what = 4.0 * S * S * Dh, "one head per call (the reference program is one head)"
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            r = subprocess.run([str(cli), "snapshots", ex, "--out-dir", d], capture_output=True, text=True, timeout=120)
+            n = json.loads(r.stdout)["snapshots"]
+            snap = 1 if (kind == "ffn" and schedule == "two_phase") else n
+            cmd = [str(cli), "run", f"{d}/snapshot_{snap}.json", "--dims", dims, "--block", "128x128", "--repeat", "4",
+                   "--precision", precision, "--route", "fused"]
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        if r.returncode != 0:
+            return {"unavailable": r.stderr.strip()[-300:]}
+        o = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"value": flops / (o["ms_mean"] / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_call": o["ms_mean"],
+                "stages_ms_best_call": o["stages_ms"], "h2d_bytes_per_step": o["h2d_bytes"],
+                "d2h_bytes_per_step": o["d2h_bytes"], "sample": what + f", mean of 3 calls after 1 (snapshot_{snap})",
+                "path": "bfgpu-cli run -> bfgpu::execute(program, map<string, MatrixXd>, binding) -> C-ABI bf_*; "
+                        "fp64 column-major in and out, conversion on the host threads"}
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        return {"unavailable": str(e)}
 
 
 # ------------------------------------------------------------------ our arm
@@ -394,17 +522,19 @@ def run_ours(args, wl):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     peaks, peaks_src = load_peaks()
+    f32 = wl["dtype"] == "f32"
 
-    inp = make_inputs(wl, rank, world, dev)
+    inp = make_inputs(wl, rank, world, dev, args.rows)
     kind = wl["kind"]
-    if kind == "ffn":
-        out = torch.empty(inp["rows"], wl["N"], dtype=torch.bfloat16, device=dev)
-    elif kind == "lnmm":
-        out = torch.empty(inp["rows"], wl["N"], dtype=torch.bfloat16, device=dev)
+    if kind in ("ffn", "lnmm"):
+        out = torch.empty(inp["rows"], wl["N"], dtype=inp["X"].dtype, device=dev)
     else:
         out = torch.empty_like(inp["Q"])
     fn = step_fn(wl, inp, args.schedule, out)
     stream = torch.cuda.current_stream(dev)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    # inputs smaller than 2x L2 (C1): flush L2 between timed steps (outside the events)
+    flush = torch.empty(2 * l2_bytes, dtype=torch.uint8, device=dev) if inp["fused_bytes"] < 2 * l2_bytes else None
 
     def barrier():
         if world > 1:
@@ -415,18 +545,42 @@ def run_ours(args, wl):
     for _ in range(args.warmup):
         fn()
     barrier()
-    launches0 = ops.kernel_launches()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        for i in range(args.steps):
+    graph_launches = 0
+    if flush is not None:
+        # A step this short (C1: ~50 us) would otherwise time the host's launch path: replay the
+        # call as a CUDA graph (the same kernel launch, captured once).
+        graph = torch.cuda.CUDAGraph()
+        n0 = ops.kernel_launches()
+        with torch.cuda.graph(graph):
             fn()
-            ev[i + 1].record(stream)
-        torch.cuda.synchronize(dev)
+        graph_launches = ops.kernel_launches() - n0
+        for _ in range(args.warmup):
+            graph.replay()
+        fn = graph.replay
+        barrier()
+    launches0 = ops.kernel_launches()
+    if flush is None:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        with ClockSampler(local) as clk:
+            ev[0].record(stream)
+            for i in range(args.steps):
+                fn()
+                ev[i + 1].record(stream)
+            torch.cuda.synchronize(dev)
+        per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    else:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            for a, b in evs:
+                flush.zero_()
+                a.record(stream)
+                fn()
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+        per_step = [a.elapsed_time(b) for a, b in evs]
     barrier()
-    launches = ops.kernel_launches() - launches0
-    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    elapsed = ev[0].elapsed_time(ev[-1])
+    launches = ops.kernel_launches() - launches0 + graph_launches * args.steps
+    elapsed = sum(per_step)
     max_elapsed_ms = max_over_ranks(elapsed, dev)
     ms_per_step = max_elapsed_ms / args.steps
     # whole-job work: every rank's units (weak scaling: world x rows_per_rank)
@@ -436,8 +590,6 @@ def run_ours(args, wl):
     # ---- end to end through the public API with pinned host buffers (e2e): ops.from_host,
     # every input copied H2D and the output D2H inside each step, overlapped with the kernels
     # row slice by row slice (weights first)
-    from paper_2505_07829_b200 import ops as _ops
-
     host = {}
     names = {"ffn": ("X", "Wt", "Vt", "Ut"), "lnmm": ("X", "Yt"), "attn": ("Q", "K", "Vt")}[kind]
     row_names = {"ffn": ("X",), "lnmm": ("X",), "attn": ("Q", "K", "Vt")}[kind]
@@ -446,13 +598,13 @@ def run_ours(args, wl):
     out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     h2d = sum(host[n].numel() * host[n].element_size() for n in names)
     d2h = out_host.numel() * out_host.element_size()
-    fn = {"ffn": _ops.rms_ffn_swiglu, "lnmm": _ops.layernorm_matmul, "attn": _ops.attention}[kind]
+    efn = {"ffn": ops.rms_ffn_swiglu, "lnmm": ops.layernorm_matmul, "attn": ops.attention}[kind]
     kw = {"schedule": args.schedule} if kind == "ffn" else {}
-    e2e_chunks = 4
+    e2e_chunks = 1 if f32 else 4
 
     def e2e_step():
-        _ops.from_host(fn, [host[n] for n in row_names], [host[n] for n in names if n not in row_names], out_host,
-                       chunks=e2e_chunks, **kw)
+        ops.from_host(efn, [host[n] for n in row_names], [host[n] for n in names if n not in row_names], out_host,
+                      chunks=e2e_chunks, **kw)
 
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
@@ -468,28 +620,20 @@ def run_ours(args, wl):
     e2e_value = total_flops / (e2e_ms / 1e3) / 1e12
 
     check = check_output(wl, inp, out) if not args.no_check else None
-    plan = None
+    pattern = {"ffn": "rms_ffn_swiglu", "lnmm": "layernorm_matmul", "attn": "attention"}[kind]
     try:
-        dims = {"ffn": lambda: (inp["rows"], wl["D"], wl["F"], wl["N"]), "lnmm": lambda: (inp["rows"], wl["K"], wl["N"]),
+        dims = {"ffn": lambda: (inp["rows"], wl["D"], wl["F"], wl["N"]),
+                "lnmm": lambda: (inp["rows"], wl["K"], wl["N"]),
                 "attn": lambda: (inp["rows"], wl["S"], wl["S"], wl["Dh"], wl["Dh"])}[kind]()
-        pattern = {"ffn": "rms_ffn_swiglu", "lnmm": "layernorm_matmul", "attn": "attention"}[kind]
-        plan = ops.plan(pattern, dims, schedule=args.schedule if kind == "ffn" else "fused", device=dev)
+        plan = ops.plan(pattern, dims, dtype=inp["X" if kind != "attn" else "Q"].dtype,
+                        schedule=args.schedule if kind == "ffn" else "fused", device=dev)
     except Exception as e:  # noqa: BLE001 - reported, not fatal
         plan = {"error": str(e)}
 
-    # ---- reference-model traffic (the reference's own traffic_bytes, metrics.hpp:154)
-    model = None
-    try:
-        from oracle import refexec as R
-
-        if R.available() and kind == "ffn":
-            M, D, F, N = inp["rows"], wl["D"], wl["F"], wl["N"]
-            b = {"M": (M // 128, 128), "N": (1, N), "K": (1, F), "D": (1, D)}
-            model = {"binding": "M in 128-row blocks, contraction dims one block (counts=1)",
-                     "fused_final_snapshot": R.traffic_bytes(2, R.FINAL, b, 2),
-                     "unfused_lowered": R.traffic_bytes(2, R.UNFUSED, b, 2)}
-    except Exception as e:  # noqa: BLE001
-        model = {"error": str(e)}
+    model = reference_model(wl, inp["rows"]) if rank == 0 else None
+    adapter = None
+    if rank == 0 and not args.no_adapter:
+        adapter = e2e_adapter(wl, inp["rows"], wl["dtype"], args.schedule)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -501,13 +645,36 @@ def run_ours(args, wl):
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        kernel_ms = ms_per_step  # one fused launch per step (fused schedule); per-rank device time
+        kernel_ms = ms_per_step  # one launch per step (fused schedule); per-rank device time
         achieved = inp["flops"] / (max_elapsed_ms / args.steps / 1e3) / 1e12
-        kkey = {"ffn": "ffn_swiglu_2sm_kernel", "lnmm": "ln_matmul_2sm_kernel", "attn": "attn_kernel"}[kind]
+        kkey = plan.get("kernel", KERNELS[kind]) if isinstance(plan, dict) else KERNELS[kind]
         capture = {"ffn": "prof_ffn" if args.schedule == "fused" else "prof_ffn2p", "lnmm": "prof_lnmm",
                    "attn": "prof_attn"}[kind]
-        if wl["name"].startswith("C5"):
+        if args.workload == "ffn_70b":
             capture = "prof_ffn70b"  # the C3 capture does not describe the 70B shape
+        elif args.workload == "lnmm_c1":
+            capture = "prof_c1"
+        if args.rows:
+            capture = None  # captures are taken at the configs' own sizes
+        traffic = ncu_traffic(f"{kkey}@{capture}") if capture else None
+        if f32:
+            peak, psrc = fp32_peak()
+            roof = {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "peak_source": psrc, "traffic": traffic, "kernel": kkey,
+                    "flops_per_launch": inp["flops"], "ms_per_launch": kernel_ms,
+                    "note": "fp32 mode runs on the FMA pipes (TF32 cannot meet the 1e-4 bar); intensity "
+                            f"{inp['flops'] / inp['fused_bytes']:.0f} FLOP/B, far above the FP32 ridge"}
+        else:
+            peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained",
+                                                              FALLBACK_PEAKS["bf16_tflops_sustained"]),
+                    "peak_source": peaks_src + ", cuBLAS bf16 burst (frac_of_sustained: the 4 s sustained figure)",
+                    "traffic": traffic, "kernel": kkey, "flops_per_launch": inp["flops"], "ms_per_launch": kernel_ms}
+        l2_note = (f"inputs {inp['fused_bytes'] / 1e6:.1f} MB < 2x L2: L2 flushed (2x L2 buffer written) before "
+                   "every timed step, outside the events; the step is a CUDA-graph replay of the call"
+                   if flush is not None else
+                   f"inputs {inp['fused_bytes'] / 1e6:.0f} MB per step > 126 MB L2; no flush needed")
         line = {
             "metric": METRIC,
             "value": value,
@@ -519,31 +686,30 @@ def run_ours(args, wl):
             "higher_is_better": True,
             "scaling": wl["scaling"],
             "vs_baseline": None,
-            "dtype": "bf16",
+            "dtype": "f32" if f32 else "bf16",
             "data": "synthetic: N(0,1) activations, N(0,1)/sqrt(fan_in) weights, seeded per rank",
             "config": {
-                "workload": wl["name"], "schedule": args.schedule if kind == "ffn" else "fused",
-                "rows_per_gpu": inp["rows"], "parallelism": f"row-sharded x{world}, no data-path collective",
-                "l2": f"inputs {inp['fused_bytes'] / 1e6:.0f} MB per step > 126 MB L2; no flush needed",
+                "workload": wl["name"] + (f" [rows/heads per GPU overridden: {args.rows}]" if args.rows else ""),
+                "schedule": args.schedule if kind == "ffn" else "fused",
+                ("heads_per_gpu" if kind == "attn" else "rows_per_gpu"): inp["rows"],
+                "parallelism": f"{'head' if kind == 'attn' else 'row'}-sharded x{world}, no data-path collective",
+                "l2": l2_note,
             },
-            "roofline": {
-                "bound": "tensor", "achieved": achieved, "peak": peaks.get("bf16_tflops"), "unit": "TFLOP/s",
-                "frac": achieved / peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]),
-                "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]),
-                "peak_source": peaks_src + ", cuBLAS bf16 burst", "traffic": ncu_traffic(f"{kkey}@{capture}"),
-                "kernel": kkey, "flops_per_launch": inp["flops"], "ms_per_launch": kernel_ms,
-            },
+            "roofline": roof,
             "hbm_bytes": {
                 "fused_algorithmic_per_gpu": inp["fused_bytes"], "unfused_op_sequence_per_gpu": inp["unfused_bytes"],
                 "unfused_over_fused": inp["unfused_bytes"] / inp["fused_bytes"], "reference_model": model,
-                "measured_ncu_per_launch": ncu_traffic(f"{kkey}@{capture}"),
-                "measured_unfused_ncu_per_step": (unfused_measured(kind) or {}).get("dram_bytes_per_step")
-                if wl["name"].startswith(("C3", "C4", "C2")) else None,
+                "measured_ncu_per_launch": traffic,
+                "measured_unfused_ncu_per_step": (unfused_measured(args.workload) or {}).get("dram_bytes_per_step")
+                if not args.rows else None,
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms, "chunks": e2e_chunks,
-                    "path": "ops.from_host -> C-ABI bf_*: pinned host buffers, every input H2D and the output D2H inside each step, overlapped with the kernels in row slices; consecutive steps alternate two device buffer sets"},
+                    "path": "ops.from_host -> C-ABI bf_*: pinned host buffers, every input H2D and the output D2H "
+                            "inside each step, overlapped with the kernels in row slices; consecutive steps "
+                            "alternate two device buffer sets"},
+            "e2e_adapter": adapter,
             "gpu_launches": launches,
             "check": check,
             "plan": plan,
@@ -564,8 +730,11 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="ffn_8b")
     ap.add_argument("--schedule", choices=["fused", "two_phase"], default="fused")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="rows (heads for attn) per GPU, overriding the workload's sharding")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip validating sampled rows of the timed output")
+    ap.add_argument("--no-adapter", action="store_true", help="skip the e2e timing through the C++ drop-in")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     wl = WORKLOADS[args.workload]

@@ -8,11 +8,16 @@
 // column-major), run the recognized kernel, and return the named output.
 #include "bfgpu_execute.hpp"
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <set>
+#include <thread>
 #include <vector>
 
 #include "bfgpu.h"
@@ -132,50 +137,139 @@ float from_bf16(uint16_t h) {
   return f;
 }
 
-// Column-major Eigen matrix -> row-major device layout (bf16 or fp32), tiled transpose.
-std::vector<uint8_t> to_device_layout(const Matrix& m, Precision prec) {
-  const long R = m.rows(), C = m.cols();
-  const size_t eb = prec == Precision::BF16 ? 2 : 4;
-  std::vector<uint8_t> buf(static_cast<size_t>(R * C) * eb);
-  constexpr long TB = 64;
-  for (long i0 = 0; i0 < R; i0 += TB)
-    for (long j0 = 0; j0 < C; j0 += TB)
-      for (long i = i0; i < std::min(R, i0 + TB); ++i)
-        for (long j = j0; j < std::min(C, j0 + TB); ++j) {
-          const float f = static_cast<float>(m(i, j));
-          if (prec == Precision::BF16)
-            reinterpret_cast<uint16_t*>(buf.data())[i * C + j] = to_bf16(f);
-          else
-            reinterpret_cast<float*>(buf.data())[i * C + j] = f;
-        }
-  return buf;
+int host_threads() {
+  static const int n = [] {
+    const char* v = std::getenv("BFGPU_HOST_THREADS");
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, v ? std::atoi(v) : std::min(hw > 0 ? hw : 1, 32));
+  }();
+  return n;
 }
 
-Matrix from_device_layout(const std::vector<uint8_t>& buf, long R, long C, Precision prec) {
-  Matrix m(R, C);
-  for (long i = 0; i < R; ++i)
-    for (long j = 0; j < C; ++j)
-      m(i, j) = prec == Precision::BF16 ? from_bf16(reinterpret_cast<const uint16_t*>(buf.data())[i * C + j])
-                                        : reinterpret_cast<const float*>(buf.data())[i * C + j];
-  return m;
+// fn(lo, hi) over [0, n) split across the host threads (the calling thread takes the first part).
+template <class Fn>
+void parallel_rows(long n, long grain, Fn fn) {
+  const long parts = std::max(1L, std::min<long>(host_threads(), (n + grain - 1) / grain));
+  if (parts == 1) {
+    fn(0L, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (long t = 1; t < parts; ++t) pool.emplace_back([&, t] { fn(n * t / parts, n * (t + 1) / parts); });
+  fn(0L, n / parts);
+  for (auto& th : pool) th.join();
+}
+
+// Column-major Eigen storage -> row-major device layout (bf16 or fp32), 32x32 tiles, row
+// bands in parallel. `dst` is page-locked so the copy that follows is asynchronous.
+void to_device_layout(const Matrix& m, Precision prec, void* dst) {
+  const long R = m.rows(), C = m.cols();
+  const double* src = m.data();
+  parallel_rows(R, 64, [&](long r0, long r1) {
+    constexpr long TB = 32;
+    for (long i0 = r0; i0 < r1; i0 += TB)
+      for (long j0 = 0; j0 < C; j0 += TB) {
+        const long i1 = std::min(r1, i0 + TB), j1 = std::min(C, j0 + TB);
+        for (long i = i0; i < i1; ++i)
+          for (long j = j0; j < j1; ++j) {
+            const float f = static_cast<float>(src[j * R + i]);
+            if (prec == Precision::BF16)
+              static_cast<uint16_t*>(dst)[i * C + j] = to_bf16(f);
+            else
+              static_cast<float*>(dst)[i * C + j] = f;
+          }
+      }
+  });
+}
+
+void from_device_layout(const void* src, Matrix& m, Precision prec) {
+  const long R = m.rows(), C = m.cols();
+  double* dst = m.data();
+  parallel_rows(C, 64, [&](long c0, long c1) {  // column bands: contiguous writes into Eigen storage
+    constexpr long TB = 32;
+    for (long j0 = c0; j0 < c1; j0 += TB)
+      for (long i0 = 0; i0 < R; i0 += TB) {
+        const long j1 = std::min(c1, j0 + TB), i1 = std::min(R, i0 + TB);
+        for (long j = j0; j < j1; ++j)
+          for (long i = i0; i < i1; ++i)
+            dst[j * R + i] = prec == Precision::BF16 ? from_bf16(static_cast<const uint16_t*>(src)[i * C + j])
+                                                     : static_cast<const float*>(src)[i * C + j];
+      }
+  });
 }
 
 void check(int rc, const char* what) {
   if (rc != BF_OK) throw Error(std::string(what) + ": " + bf_last_error());
 }
 
-struct DeviceBuffer {
+// Grow-only buffers, cached per thread and device: concurrent execute() calls (allowed by the
+// reference contract) never share one, and repeated calls of one shape allocate
+// nothing. Every call ends with a stream synchronize, so reuse by the next call is safe.
+struct HostBuf {
   void* p = nullptr;
-  explicit DeviceBuffer(size_t bytes) {
-    p = bf_device_alloc(bytes);
-    if (!p) throw Error(std::string("device allocation failed: ") + bf_last_error());
+  size_t n = 0;
+  ~HostBuf() {
+    if (p) bf_host_free(p);
   }
-  ~DeviceBuffer() {
+  void* get(size_t bytes) {
+    if (bytes > n) {
+      if (p) bf_host_free(p);
+      p = bf_host_alloc(bytes);
+      if (!p) throw Error(std::string("pinned host allocation failed: ") + bf_last_error());
+      n = bytes;
+    }
+    return p;
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
     if (p) bf_device_free(p);
   }
-  DeviceBuffer(const DeviceBuffer&) = delete;
-  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  void* get(size_t bytes) {
+    if (bytes > n) {
+      if (p) bf_device_free(p);
+      p = bf_device_alloc(bytes);
+      if (!p) throw Error(std::string("device allocation failed: ") + bf_last_error());
+      n = bytes;
+    }
+    return p;
+  }
 };
+
+struct Staging {
+  std::map<std::string, HostBuf> host;
+  std::map<std::pair<int, std::string>, DevBuf> dev;
+  int device = 0;
+  void* stream = nullptr;
+  // Convert into a pinned buffer, then queue its asynchronous copy: the copy of one input
+  // overlaps the conversion of the next.
+  void* upload(const std::string& name, const Matrix& m, Precision prec) {
+    const size_t bytes = static_cast<size_t>(m.rows() * m.cols()) * (prec == Precision::BF16 ? 2 : 4);
+    void* h = host[name].get(bytes);
+    to_device_layout(m, prec, h);
+    void* d = dev[{device, name}].get(bytes);
+    check(bf_copy_to_device(d, h, bytes, stream), "copy to device");
+    return d;
+  }
+  void* scratch(const std::string& name, size_t bytes) { return dev[{device, name}].get(bytes); }
+};
+
+Staging& staging(void* stream) {
+  thread_local Staging st;
+  st.device = bf_get_device();
+  if (st.device < 0) throw Error(std::string("no CUDA device: ") + bf_last_error());
+  st.stream = stream;
+  return st;
+}
+
+thread_local ExecTiming t_timing;
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 // Named input checked against the binding the way eval_graph's Input case does (interpreter.hpp:386-403).
 const Matrix& input(const std::map<std::string, Matrix>& in, const std::string& name, long rows, long cols) {
@@ -186,20 +280,36 @@ const Matrix& input(const std::map<std::string, Matrix>& in, const std::string& 
   return it->second;
 }
 
-struct Staged {
-  std::vector<std::unique_ptr<DeviceBuffer>> bufs;
-  void* upload(const Matrix& m, Precision prec, void* stream) {
-    std::vector<uint8_t> host = to_device_layout(m, prec);
-    bufs.push_back(std::make_unique<DeviceBuffer>(host.size()));
-    check(bf_copy_to_device(bufs.back()->p, host.data(), host.size(), stream), "copy to device");
-    check(bf_stream_synchronize(stream), "stream synchronize");  // `host` is pageable and goes out of scope
-    return bufs.back()->p;
+// Why the fused kernel cannot take this recognized program at this binding and precision
+// (empty: it can). Mirrors the argument checks of the C-ABI entry points.
+std::string unsupported_reason(const Recognized& r, const DimBinding& b, Precision prec) {
+  if (r.pattern == Pattern::Attention) {
+    const long D = b.total("D"), L = b.total("L"), N = b.total("N");
+    if (prec == Precision::F32) return D <= 256 && L <= 256 ? "" : "fp32 attention needs head dims <= 256";
+    if ((D != 64 && D != 128) || (L != 64 && L != 128)) return "bf16 attention needs head dims D, L in {64, 128}";
+    if (N % 8) return "bf16 attention needs the key count a multiple of 8";
+    return "";
   }
-  void* alloc(size_t bytes) {
-    bufs.push_back(std::make_unique<DeviceBuffer>(bytes));
-    return bufs.back()->p;
+  if (prec == Precision::F32) return "";
+  if (r.pattern == Pattern::LayerNormMatMul) {
+    if (b.total("K") % 8 || b.total("N") % 8) return "bf16 layernorm_matmul needs K and N multiples of 8";
+    return "";
   }
-};
+  if (b.total("D") % 8 || b.total("K") % 8 || b.total("N") % 8)
+    return "bf16 rms_ffn_swiglu needs D, F (dim K) and N multiples of 8";
+  return "";
+}
+
+// Auto-route fallbacks are reported once per reason on stderr (BFGPU_QUIET=1 silences them).
+void note_fallback(const std::string& why) {
+  static std::mutex mu;
+  static std::set<std::string> seen;
+  const char* q = std::getenv("BFGPU_QUIET");
+  if (q && q[0] == '1') return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (seen.insert(why).second)
+    std::fprintf(stderr, "bfgpu::execute: %s; running it on the generic float64 GPU route\n", why.c_str());
+}
 
 Precision env_precision() {
   const char* v = std::getenv("BFGPU_PRECISION");
@@ -254,64 +364,94 @@ std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const st
   Recognized rec;
   try {
     rec = recognize(program);
-  } catch (const Error&) {
+  } catch (const Error& e) {
     if (cfg.route == Route::Fused) throw;
+    note_fallback("program is not a recognized fused candidate");
+    return execute_generic(program, inputs, binding, opts, cfg.stream);
+  }
+  const std::string why = unsupported_reason(rec, binding, cfg.precision);
+  if (!why.empty()) {
+    if (cfg.route == Route::Fused) throw Error("bfgpu::execute: " + why);
+    note_fallback(why);
     return execute_generic(program, inputs, binding, opts, cfg.stream);
   }
   const int dt = cfg.precision == Precision::BF16 ? BF_DTYPE_BF16 : BF_DTYPE_F32;
   const size_t eb = cfg.precision == Precision::BF16 ? 2 : 4;
   void* s = cfg.stream;
-  Staged st;
+  Staging& st = staging(s);
+  ExecTiming tm;
+  const double t0 = now_ms();
   long out_rows = 0, out_cols = 0;
   void* out = nullptr;
   switch (rec.pattern) {
     case Pattern::RmsFfnSwiglu: {
       const long M = binding.total("M"), D = binding.total("D"), F = binding.total("K"), N = binding.total("N");
-      void* X = st.upload(input(inputs, "X", M, D), cfg.precision, s);
-      void* Wt = st.upload(input(inputs, "Wt", F, D), cfg.precision, s);
-      void* Vt = st.upload(input(inputs, "Vt", F, D), cfg.precision, s);
-      void* Ut = st.upload(input(inputs, "Ut", N, F), cfg.precision, s);
+      const Matrix& x = input(inputs, "X", M, D);
+      const Matrix& wt = input(inputs, "Wt", F, D);
+      const Matrix& vt = input(inputs, "Vt", F, D);
+      const Matrix& ut = input(inputs, "Ut", N, F);
+      void* X = st.upload("X", x, cfg.precision);
+      void* Wt = st.upload("Wt", wt, cfg.precision);
+      void* Vt = st.upload("Vt", vt, cfg.precision);
+      void* Ut = st.upload("Ut", ut, cfg.precision);
+      tm.convert_in_ms = now_ms() - t0;
       out_rows = M;
       out_cols = N;
-      out = st.alloc(static_cast<size_t>(M * N) * eb);
+      out = st.scratch("O", static_cast<size_t>(M * N) * eb);
       const int sched = rec.materializes_intermediate ? BF_FFN_TWO_PHASE : BF_FFN_FUSED;
       const size_t wsb = bf_rms_ffn_swiglu_workspace_bytes(M, D, F, N, dt, sched);
-      void* ws = st.alloc(wsb);
+      void* ws = st.scratch("ws", wsb);
       check(bf_rms_ffn_swiglu(X, Wt, Vt, Ut, out, M, D, F, N, dt, static_cast<float>(rec.eps), sched, ws, wsb, s),
             "bf_rms_ffn_swiglu");
       break;
     }
     case Pattern::LayerNormMatMul: {
       const long M = binding.total("M"), K = binding.total("K"), N = binding.total("N");
-      void* X = st.upload(input(inputs, "X", M, K), cfg.precision, s);
-      void* Yt = st.upload(input(inputs, "Yt", N, K), cfg.precision, s);
+      void* X = st.upload("X", input(inputs, "X", M, K), cfg.precision);
+      void* Yt = st.upload("Yt", input(inputs, "Yt", N, K), cfg.precision);
+      tm.convert_in_ms = now_ms() - t0;
       out_rows = M;
       out_cols = N;
-      out = st.alloc(static_cast<size_t>(M * N) * eb);
+      out = st.scratch("O", static_cast<size_t>(M * N) * eb);
       const size_t wsb = bf_layernorm_matmul_workspace_bytes(M, K, N, dt);
-      void* ws = st.alloc(wsb);
+      void* ws = st.scratch("ws", wsb);
       check(bf_layernorm_matmul(X, Yt, out, M, K, N, dt, 0.0f, ws, wsb, s), "bf_layernorm_matmul");
       break;
     }
     case Pattern::Attention: {
       const long M = binding.total("M"), N = binding.total("N"), D = binding.total("D"), L = binding.total("L");
-      void* Q = st.upload(input(inputs, "Q", M, D), cfg.precision, s);
-      void* K = st.upload(input(inputs, "K", N, D), cfg.precision, s);
-      void* Vt = st.upload(input(inputs, "Vt", L, N), cfg.precision, s);
+      void* Q = st.upload("Q", input(inputs, "Q", M, D), cfg.precision);
+      void* K = st.upload("K", input(inputs, "K", N, D), cfg.precision);
+      void* Vt = st.upload("Vt", input(inputs, "Vt", L, N), cfg.precision);
+      tm.convert_in_ms = now_ms() - t0;
       out_rows = M;
       out_cols = L;
-      out = st.alloc(static_cast<size_t>(M * L) * eb);
+      out = st.scratch("O", static_cast<size_t>(M * L) * eb);
       check(bf_attention(Q, K, Vt, out, 1, M, N, D, L, dt, 0.0f, s), "bf_attention");  // scale 1/sqrt(total(D))
       break;
     }
   }
-  std::vector<uint8_t> host(static_cast<size_t>(out_rows * out_cols) * eb);
-  check(bf_copy_to_host(host.data(), out, host.size(), s), "copy to host");
+  const size_t out_bytes = static_cast<size_t>(out_rows * out_cols) * eb;
+  void* host_out = st.host["O"].get(out_bytes);
+  check(bf_copy_to_host(host_out, out, out_bytes, s), "copy to host");
+  const double t1 = now_ms();
   check(bf_stream_synchronize(s), "stream synchronize");
+  const double t2 = now_ms();
+  tm.device_ms = t2 - t1;
   std::map<std::string, Matrix> result;
-  result[rec.output] = from_device_layout(host, out_rows, out_cols, cfg.precision);
+  Matrix& o = result[rec.output];
+  o.resize(out_rows, out_cols);
+  from_device_layout(host_out, o, cfg.precision);
+  tm.convert_out_ms = now_ms() - t2;
+  tm.total_ms = now_ms() - t0;
+  tm.h2d_bytes = 0;
+  for (const auto& [n, m] : inputs) tm.h2d_bytes += static_cast<size_t>(m.rows() * m.cols()) * eb;
+  tm.d2h_bytes = out_bytes;
+  t_timing = tm;
   return result;
 }
+
+const ExecTiming& last_timing() { return t_timing; }
 
 std::map<std::string, Matrix> execute(const BlockGraph& program, const std::map<std::string, Matrix>& inputs,
                                       const DimBinding& binding, const blockfuse::ExecOptions& opts) {

@@ -50,6 +50,17 @@ struct Recognized {
   std::string output;                   // name of the Output node
 };
 
+// Where the time of the calling thread's last execute() on a fused kernel went.
+struct ExecTiming {
+  double convert_in_ms = 0;   // column-major float64 -> row-major bf16/fp32 into pinned memory (host threads),
+                              // overlapped with the asynchronous uploads of the inputs before it
+  double device_ms = 0;       // remaining uploads + kernel + download, after the last conversion
+  double convert_out_ms = 0;  // widening the output back into the Eigen matrix
+  double total_ms = 0;
+  size_t h2d_bytes = 0, d2h_bytes = 0;
+};
+const ExecTiming& last_timing();
+
 // Identifies `program` as one of the reference fusion driver's snapshots by the
 // reference's own isomorphism test (canonical_form, serialize.hpp:370).
 // Throws blockfuse::Error for anything else.

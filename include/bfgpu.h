@@ -59,11 +59,14 @@ extern "C" {
 #define BF_DTYPE_BF16 0
 #define BF_DTYPE_F32 1
 
-/* K1 schedules. FUSED runs the whole program in one persistent kernel: the
- * SwiGLU intermediate H travels through an L2-resident ring and is never
- * written back to HBM in steady state (final snapshot, interpreter.hpp walk
- * of fuse(lower(rms_ffn_swiglu()))). TWO_PHASE is the reference's first
- * fusion snapshot (one internal buffered edge: H materialized in HBM). */
+/* K1 schedules. FUSED runs the whole program in one persistent kernel (final
+ * snapshot of fuse(lower(rms_ffn_swiglu()))): gate/up tiles hand H to the
+ * down tiles of the same m-unit inside the launch, through a workspace slab
+ * that the planner sizes per scheduling group to fit L2. H is not re-read
+ * from HBM by a second launch, but at d=4096 and above the slabs of the two
+ * groups in flight exceed L2, so part of H is written back (K1 DRAM
+ * floor). TWO_PHASE is the reference's first fusion snapshot (one internal
+ * buffered edge: H materialized in HBM between two launches). */
 #define BF_FFN_FUSED 0
 #define BF_FFN_TWO_PHASE 1
 
@@ -160,6 +163,12 @@ BF_API int bf_device_free(void* ptr);
 BF_API int bf_copy_to_device(void* dst, const void* src, size_t bytes, void* stream);
 BF_API int bf_copy_to_host(void* dst, const void* src, size_t bytes, void* stream);
 BF_API int bf_stream_synchronize(void* stream);
+/* Page-locked host memory (cudaHostAlloc, portable): staging for asynchronous copies. */
+BF_API void* bf_host_alloc(size_t bytes);
+BF_API int bf_host_free(void* ptr);
+/* Current device of the calling thread (-1 on error) / select it. */
+BF_API int bf_get_device(void);
+BF_API int bf_set_device(int device);
 
 /* ------------------------------------------------------------------------
  * Device memory / tile planner
@@ -178,6 +187,41 @@ BF_API int bf_stream_synchronize(void* stream);
 #define BF_PATTERN_ATTENTION 2
 BF_API int bf_plan_json(int pattern, const int64_t* dims, int ndims, int dtype, int schedule, char* buf,
                         size_t len);
+
+/* ------------------------------------------------------------------------
+ * Row/head-sharded multi-GPU launch (one host thread, N devices)
+ *   The fused programs shard with no exchange step: rows of X for
+ *   RMS_FFN_SWIGLU / LAYERNORM_MATMUL (per-row statistics; the M map is a
+ *   forall, interpreter.hpp:334) and heads for ATTENTION. Shard g covers units
+ *   [start, stop) of bf_shard_range (128-row aligned for rows, whole heads),
+ *   runs on io[g].device with that device's pointers, and nothing crosses
+ *   devices unless gather != 0: then every io[g].out_full receives the whole
+ *   output (an all-gather-v: NCCL broadcasts from each shard's owner in one
+ *   group over NVLink/NVSwitch when the devices are distinct, peer copies
+ *   otherwise; BFGPU_GATHER=nccl|peer forces one). Reentrant per device set;
+ *   concurrent execute() calls of the reference contract map to
+ *   independent calls of this function.
+ * Replaces: nothing in the reference (its executor is single-threaded on one
+ *   host); it is the multi-GPU form of execute() for the three programs.
+ * dims are the WHOLE problem's (as bf_plan_json); io[g].in[] are the shard's
+ *   operands on its device: K1 {X rows, Wt, Vt, Ut}, K2 {X rows, Yt},
+ *   K3 {Q, K, Vt of the shard's heads}; io[g].out the shard's output.
+ *   eps_or_scale: rmsnorm/layernorm eps (K1, K2) or the softmax scale (K3).
+ * ---------------------------------------------------------------------- */
+typedef struct bf_shard_io {
+  int device;
+  const void* in[4];
+  void* out;
+  void* out_full;
+  void* workspace;
+  size_t workspace_bytes;
+  void* stream;
+} bf_shard_io;
+BF_API int bf_shard_range(int pattern, int64_t units, int ngpu, int shard, int64_t* start, int64_t* stop);
+BF_API int bf_launch_sharded(int pattern, int ngpu, const bf_shard_io* io, const int64_t* dims, int ndims, int dtype,
+                             int schedule, float eps_or_scale, int gather);
+/* NCCL version found at run time (libnccl.so.2 via dlopen), or -1 if none. */
+BF_API int bf_nccl_version(void);
 
 /* ------------------------------------------------------------------------
  * Introspection

@@ -65,6 +65,10 @@ _SIGNATURES = [
     ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_copy_to_host", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_stream_synchronize", ctypes.c_int, [_vp]),
+    ("bf_host_alloc", ctypes.c_void_p, [ctypes.c_size_t]),
+    ("bf_host_free", ctypes.c_int, [_vp]),
+    ("bf_get_device", ctypes.c_int, []),
+    ("bf_set_device", ctypes.c_int, [ctypes.c_int]),
     ("bf_plan_json", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_i64), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_char_p, ctypes.c_size_t]),
     ("bf_last_error", ctypes.c_char_p, []),
@@ -109,3 +113,21 @@ def lib():
 def check(code: int) -> None:
     if code != BF_OK:
         raise BfError(code, lib().bf_last_error().decode(errors="replace"))
+
+
+class ShardIO(ctypes.Structure):
+    """bf_shard_io (include/bfgpu.h): one shard's device, operands, output and stream."""
+
+    _fields_ = [("device", ctypes.c_int), ("in_", ctypes.c_void_p * 4), ("out", ctypes.c_void_p),
+                ("out_full", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("stream", ctypes.c_void_p)]
+
+
+_SIGNATURES += [
+    ("bf_shard_range", ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i64),
+                                      ctypes.POINTER(_i64)]),
+    ("bf_launch_sharded", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ShardIO), ctypes.POINTER(_i64),
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_int]),
+    ("bf_nccl_version", ctypes.c_int, []),
+]
+EXPORTED = [s[0] for s in _SIGNATURES]

@@ -177,4 +177,23 @@ int bf_stream_synchronize(void* stream) {
   return guarded([&] { BF_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
 }
 
+void* bf_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  const int rc = guarded([&] { BF_CUDA(cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable)); });
+  return rc == BF_OK ? p : nullptr;
+}
+
+int bf_host_free(void* ptr) {
+  return guarded([&] { BF_CUDA(cudaFreeHost(ptr)); });
+}
+
+int bf_get_device(void) {
+  int d = -1;
+  return guarded([&] { BF_CUDA(cudaGetDevice(&d)); }) == BF_OK ? d : -1;
+}
+
+int bf_set_device(int device) {
+  return guarded([&] { BF_CUDA(cudaSetDevice(device)); });
+}
+
 }  // extern "C"

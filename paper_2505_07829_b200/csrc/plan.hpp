@@ -79,9 +79,9 @@ void ensure_smem_attr(const void* func, int bytes);
 // CTAs of `k` that fit on the device at once (cluster-aware occupancy), cached per device.
 int resident_ctas(const KernelSpec& k);
 
-Plan plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule);
-Plan plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype);
-Plan plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype);
+const Plan& plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule);
+const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype);
+const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype);
 std::string plan_json(const Plan& p);
 
 // Kernel descriptors, defined next to each kernel.

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <set>
 #include <sstream>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -125,7 +126,7 @@ int resident_ctas(const KernelSpec& k) {
 }
 
 // ------------------------------------------------------------------ K1
-Plan plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule) {
+static Plan make_plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule) {
   Plan p;
   p.pattern = kPatFfn;
   p.dtype = dtype;
@@ -199,7 +200,7 @@ Plan plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedul
 }
 
 // ------------------------------------------------------------------ K2
-Plan plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
+static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
   Plan p;
   p.pattern = kPatLnmm;
   p.dtype = dtype;
@@ -248,7 +249,7 @@ Plan plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
 }
 
 // ------------------------------------------------------------------ K3
-Plan plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype) {
+static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype) {
   Plan p;
   p.pattern = kPatAttn;
   p.dtype = dtype;
@@ -283,6 +284,41 @@ Plan plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, 
   p.notes = why.str();
   check_budgets(p);
   return p;
+}
+
+// Plans are pure functions of (pattern, shape, dtype, schedule, device) and the process's
+// environment overrides: cache them, so a launch costs a map lookup, not a plan.
+namespace {
+using PlanKey = std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int>;
+
+template <class Make>
+const Plan& cached_plan(const PlanKey& key, Make make) {
+  static std::mutex mu;
+  static std::map<PlanKey, Plan> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  Plan p = make();
+  std::lock_guard<std::mutex> lk(mu);
+  return cache.emplace(key, std::move(p)).first->second;
+}
+}  // namespace
+
+const Plan& plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule) {
+  return cached_plan(PlanKey{kPatFfn, M, D, F, N, 0, dtype, schedule, current_device()},
+                     [&] { return make_plan_ffn(M, D, F, N, dtype, schedule); });
+}
+
+const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
+  return cached_plan(PlanKey{kPatLnmm, M, K, N, 0, 0, dtype, 0, current_device()},
+                     [&] { return make_plan_lnmm(M, K, N, dtype); });
+}
+
+const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype) {
+  return cached_plan(PlanKey{kPatAttn, BH, Sq, Skv, D, Dv, dtype, 0, current_device()},
+                     [&] { return make_plan_attention(BH, Sq, Skv, D, Dv, dtype); });
 }
 
 std::string plan_json(const Plan& p) {

@@ -22,114 +22,246 @@ extern void note_launch();
 
 namespace simt {
 
-constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256;
+constexpr int BM = 64, BK = 16, THREADS = 128;
+constexpr int TM = 8;  // rows per thread (8 thread rows x 8 = 64)
 
 enum Epi : int { kPlain = 0, kSwiGLU = 1, kLNMM = 2 };
+
+// Output columns per CTA: 128 for one B operand (8 per thread), 64 per operand for the
+// SwiGLU tile (4 per thread per operand, gate and up side by side).
+template <int EPI>
+struct Shape {
+  static constexpr int NB = EPI == kSwiGLU ? 2 : 1;  // B operands
+  static constexpr int BN = EPI == kSwiGLU ? 64 : 128;
+  static constexpr int TN = BN / 16;  // columns per thread per operand (16 thread columns)
+};
 
 struct EpiParams {
   float inv_k;  // 1/total(K) of the normalized operand
   float eps;
 };
 
-// C[M,N] = epilogue(A[M,K] . B[N,K]^T (, A . B2^T)), all row-major fp32.
+// A register pair {lo, hi} for the packed FP32 pipe (no integer ops: a 64-bit register view).
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
+// d = a * b + d on a pair of fp32 lanes (FFMA2: one issue slot for two FMAs on sm_100).
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
+// Loads a float4 of row `r` (< rows), columns [k, k+4) of a [rows, K] row-major matrix,
+// zero-filling past the edges (vector path when K % 4 == 0).
+__device__ __forceinline__ float4 load4(const float* __restrict__ base, int r, int rows, int k, int K, bool vec) {
+  if (r >= rows) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* p = base + static_cast<size_t>(r) * K + k;
+  if (vec && k + 3 < K) return __ldg(reinterpret_cast<const float4*>(p));
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = k + i < K ? __ldg(p + i) : 0.f;
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// C[M, N] = epilogue(A[M,K] . B[N,K]^T (, A . B2^T)), all row-major fp32 (K-major operands, the
+// reference's dot convention, interpreter.hpp:289-294).
+// 128 threads, 64 x BN tile, BK = 16; each thread owns 8 rows x TN columns per operand, issued as
+// FFMA2 pairs along n (per K step: 2 LDS.128 of A, broadcast, and TN/4 LDS.128 of B per operand
+// for 4*TN*NB FFMA2: the SMEM pipe stays below the FMA pipe). The next K slice is prefetched into
+// registers while the current one is consumed from SMEM (two SMEM buffers, one barrier per
+// slice). Row statistics and colsum(Yt) are taken from the staging registers as the tiles
+// stream past: no extra SMEM reads.
 template <int EPI>
 __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                            const float* __restrict__ B2, float* __restrict__ C, int M,
                                                            int N, int K, EpiParams ep) {
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
-  __shared__ float B2s[EPI == kSwiGLU ? BK : 1][BN + 4];
-  __shared__ float row_s1[BM], row_s2[BM], row_piv[BM], col_s[BN];
+  using S = Shape<EPI>;
+  constexpr int NB = S::NB, BN = S::BN, TN = S::TN;
+  constexpr int APAD = BM + 4, BPAD = BN + 4;
+  constexpr int ALOADS = BM * BK / 4 / THREADS;  // float4 loads of A per thread (2)
+  constexpr int BLOADS = BN * BK / 4 / THREADS;  // float4 loads of each B operand per thread
+  __shared__ __align__(16) float As[2][BK][APAD];
+  __shared__ __align__(16) float Bs[2][NB][BK][BPAD];
+  __shared__ float row_a[BM], row_b[BM], col_s[BN];
 
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const bool vec = (K % 4) == 0;
+  const float* Bop[2] = {B, B2};
 
-  float acc[4][4] = {};
-  float acc2[4][4] = {};
-  float s1 = 0.f, s2 = 0.f, cs = 0.f;  // stats owned by threads < 64 (rows) and 64..127 (cols)
-  // K2 moments are taken about the row's first element (shifted moments: no E[x^2] - mu^2
-  // cancellation when |mean| >> sigma); K1 needs the plain sum of squares.
-  // For K2 the contraction runs on the shifted rows too: (X - p) Yt^T - (mu - p) colsum(Yt) is
-  // the same value as X Yt^T - mu colsum(Yt), without the fp32 cancellation of two large terms.
-  if (EPI == kLNMM && tid < BM) row_piv[tid] = m0 + tid < M ? A[static_cast<size_t>(m0 + tid) * K] : 0.f;
-  if constexpr (EPI == kLNMM) __syncthreads();
+  // staging assignment: rows lr + 32 i of A and of each B operand, K quad kq
+  const int lr = tid / 4, kq = (tid % 4) * 4;
+  // K2: rows are shifted by a pivot (their first element) before the statistics and the
+  // contraction: (X - p) Yt^T - (mu - p) colsum(Yt) equals X Yt^T - mu colsum(Yt) without the
+  // fp32 cancellation when |mu| >> sigma, and so do the moments.
+  float piv[ALOADS];
+#pragma unroll
+  for (int i = 0; i < ALOADS; ++i) {
+    const int r = m0 + lr + 32 * i;
+    piv[i] = (EPI == kLNMM && r < M) ? __ldg(A + static_cast<size_t>(r) * K) : 0.f;
+  }
+  float st1[ALOADS] = {}, st2[ALOADS] = {};  // this thread's share of its rows' moments
+  float cs[BLOADS] = {};                     // this thread's share of colsum(Yt) rows
+  float4 ra[ALOADS], rb[NB][BLOADS];
 
-  for (int k0 = 0; k0 < K; k0 += BK) {
-    for (int i = tid; i < BM * BK; i += THREADS) {
-      const int r = i / BK, c = i % BK;
-      const int gm = m0 + r, gk = k0 + c;
-      As[c][r] = (gm < M && gk < K) ? A[static_cast<size_t>(gm) * K + gk] - (EPI == kLNMM ? row_piv[r] : 0.f) : 0.f;
-      const int gn = n0 + r;
-      Bs[c][r] = (gn < N && gk < K) ? B[static_cast<size_t>(gn) * K + gk] : 0.f;
-      if constexpr (EPI == kSwiGLU) B2s[c][r] = (gn < N && gk < K) ? B2[static_cast<size_t>(gn) * K + gk] : 0.f;
-    }
-    __syncthreads();
-    if constexpr (EPI != kPlain) {
-      if (tid < BM) {
+  auto fetch = [&](int k0) {
 #pragma unroll
-        for (int c = 0; c < BK; ++c) {
-          const float x = As[c][tid];  // zero past K (and already shifted for K2)
-          s1 += x;
-          s2 = fmaf(x, x, s2);
-        }
-      } else if (EPI == kLNMM && tid < BM + BN) {
-#pragma unroll
-        for (int c = 0; c < BK; ++c) cs += Bs[c][tid - BM];
+    for (int i = 0; i < ALOADS; ++i) {
+      ra[i] = load4(A, m0 + lr + 32 * i, M, k0 + kq, K, vec);
+      if (EPI == kLNMM && m0 + lr + 32 * i < M) {
+        // padding lanes past K stay 0 (not -p): only real elements are shifted
+        if (k0 + kq + 0 < K) ra[i].x -= piv[i];
+        if (k0 + kq + 1 < K) ra[i].y -= piv[i];
+        if (k0 + kq + 2 < K) ra[i].z -= piv[i];
+        if (k0 + kq + 3 < K) ra[i].w -= piv[i];
       }
     }
+#pragma unroll
+    for (int o = 0; o < NB; ++o)
+#pragma unroll
+      for (int i = 0; i < BLOADS; ++i) rb[o][i] = load4(Bop[o], n0 + lr + 32 * i, N, k0 + kq, K, vec);
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < ALOADS; ++i) {
+      const int r = lr + 32 * i;
+      As[buf][kq + 0][r] = ra[i].x;
+      As[buf][kq + 1][r] = ra[i].y;
+      As[buf][kq + 2][r] = ra[i].z;
+      As[buf][kq + 3][r] = ra[i].w;
+      if (EPI != kPlain) {
+        st1[i] += (ra[i].x + ra[i].y) + (ra[i].z + ra[i].w);
+        st2[i] = fmaf(ra[i].x, ra[i].x, fmaf(ra[i].y, ra[i].y, fmaf(ra[i].z, ra[i].z, fmaf(ra[i].w, ra[i].w, st2[i]))));
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NB; ++o)
+#pragma unroll
+      for (int i = 0; i < BLOADS; ++i) {
+        const int c = lr + 32 * i;
+        Bs[buf][o][kq + 0][c] = rb[o][i].x;
+        Bs[buf][o][kq + 1][c] = rb[o][i].y;
+        Bs[buf][o][kq + 2][c] = rb[o][i].z;
+        Bs[buf][o][kq + 3][c] = rb[o][i].w;
+        if (EPI == kLNMM) cs[i] += (rb[o][i].x + rb[o][i].y) + (rb[o][i].z + rb[o][i].w);
+      }
+  };
+
+  unsigned long long acc[NB][TM][TN / 2];
+#pragma unroll
+  for (int o = 0; o < NB; ++o)
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN / 2; ++j) acc[o][i][j] = 0ull;
+
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    const bool more = k0 + BK < K;
+    if (more) fetch(k0 + BK);
 #pragma unroll
     for (int c = 0; c < BK; ++c) {
-      float a[4], b[4], b2[4];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][c][ty * TM]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][c][ty * TM + 4]);
+      const unsigned long long a2[TM] = {pack2(a0.x, a0.x), pack2(a0.y, a0.y), pack2(a0.z, a0.z), pack2(a0.w, a0.w),
+                                         pack2(a1.x, a1.x), pack2(a1.y, a1.y), pack2(a1.z, a1.z), pack2(a1.w, a1.w)};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i] = As[c][ty * 4 + i];
-        b[i] = Bs[c][tx * 4 + i];
-        if constexpr (EPI == kSwiGLU) b2[i] = B2s[c][tx * 4 + i];
-      }
+      for (int o = 0; o < NB; ++o) {
+        unsigned long long b2[TN / 2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-          if constexpr (EPI == kSwiGLU) acc2[i][j] = fmaf(a[i], b2[j], acc2[i][j]);
+        for (int j = 0; j < TN / 4; ++j) {
+          const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][o][c][tx * TN + 4 * j]);
+          b2[2 * j] = pack2(b4.x, b4.y);
+          b2[2 * j + 1] = pack2(b4.z, b4.w);
         }
-    }
-    __syncthreads();
-  }
-  if constexpr (EPI != kPlain) {
-    if (tid < BM) {
-      row_s1[tid] = s1;
-      row_s2[tid] = s2;
-    } else if (EPI == kLNMM && tid < BM + BN) {
-      col_s[tid - BM] = cs;
-    }
-    __syncthreads();
-  }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = ty * 4 + i, gm = m0 + r;
-    if (gm >= M) continue;
-    float scale = 1.f, mu = 0.f;
-    if constexpr (EPI == kSwiGLU) scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k + ep.eps);
-    if constexpr (EPI == kLNMM) {
-      const float dm = row_s1[r] * ep.inv_k;
-      mu = dm;  // the accumulator holds (X - p) Yt^T: subtract (mu - p) colsum(Yt)
-      // var = t2/total(K) + (0 - square(t1/total(K)))   (fused program), moments about the pivot
-      scale = 1.0f / sqrtf(row_s2[r] * ep.inv_k - dm * dm + ep.eps);
-    }
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = tx * 4 + j, gn = n0 + c;
-      if (gn >= N) continue;
-      float v = acc[i][j];
-      if constexpr (EPI == kSwiGLU) {
-        const float g = scale * v, u = scale * acc2[i][j];
-        v = g / (1.0f + expf(-g)) * u;
-      } else if constexpr (EPI == kLNMM) {
-        v = (v - mu * col_s[c]) * scale;
+          for (int j = 0; j < TN / 2; ++j) ffma2(acc[o][i][j], a2[i], b2[j]);
       }
-      C[static_cast<size_t>(gm) * N + gn] = v;
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+
+  if constexpr (EPI != kPlain) {
+    // the 4 lanes sharing a row (tid % 4) hold its quarters
+#pragma unroll
+    for (int i = 0; i < ALOADS; ++i) {
+      st1[i] += __shfl_xor_sync(0xffffffffu, st1[i], 1);
+      st1[i] += __shfl_xor_sync(0xffffffffu, st1[i], 2);
+      st2[i] += __shfl_xor_sync(0xffffffffu, st2[i], 1);
+      st2[i] += __shfl_xor_sync(0xffffffffu, st2[i], 2);
+    }
+    if constexpr (EPI == kLNMM) {
+#pragma unroll
+      for (int i = 0; i < BLOADS; ++i) {
+        cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 1);
+        cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 2);
+      }
+    }
+    if ((tid & 3) == 0) {
+#pragma unroll
+      for (int i = 0; i < ALOADS; ++i) {
+        const int r = lr + 32 * i;
+        if constexpr (EPI == kSwiGLU) {
+          row_a[r] = 1.0f / sqrtf(st2[i] * ep.inv_k + ep.eps);  // r (rmsnorm scale, lowering.hpp:409-411)
+        } else {
+          const float dm = st1[i] * ep.inv_k;  // mean of the shifted row
+          row_a[r] = dm;
+          // var = t2/total(K) + (0 - square(t1/total(K)))  (fused program), about the pivot
+          row_b[r] = 1.0f / sqrtf(st2[i] * ep.inv_k - dm * dm + ep.eps);
+        }
+      }
+      if constexpr (EPI == kLNMM) {
+#pragma unroll
+        for (int i = 0; i < BLOADS; ++i) col_s[lr + 32 * i] = cs[i];
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int r = ty * TM + i, gm = m0 + r;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN / 2; ++j) {
+      const float2 g2 = unpack2(acc[0][i][j]);
+      float v[2] = {g2.x, g2.y};
+      if constexpr (EPI == kSwiGLU) {
+        const float2 u2 = unpack2(acc[NB - 1][i][j]);
+        const float u[2] = {u2.x, u2.y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float g = row_a[r] * v[e];
+          v[e] = g / (1.0f + expf(-g)) * (row_a[r] * u[e]);
+        }
+      } else if constexpr (EPI == kLNMM) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) v[e] = (v[e] - row_a[r] * col_s[tx * TN + 2 * j + e]) * row_b[r];
+      }
+      const int gn = n0 + tx * TN + 2 * j;
+      float* dst = C + static_cast<size_t>(gm) * N + gn;
+      if (gn + 1 < N && (N % 2) == 0) {
+        *reinterpret_cast<float2*>(dst) = make_float2(v[0], v[1]);
+      } else {
+        if (gn < N) dst[0] = v[0];
+        if (gn + 1 < N) dst[1] = v[1];
+      }
     }
   }
 }
@@ -221,8 +353,10 @@ __global__ void __launch_bounds__(ATHREADS) attn_f32_kernel(const float* __restr
 template <int EPI>
 void launch_gemm(const float* A, const float* B, const float* B2, float* C, int64_t M, int64_t N, int64_t K,
                  EpiParams ep, cudaStream_t s) {
+  constexpr int BN = Shape<EPI>::BN;
   dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
   BF_CHECK_ARG(grid.y <= 65535, "fp32 mode: M too large");
+  BF_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "fp32 mode: dimension too large");
   gemm_f32_kernel<EPI><<<grid, THREADS, 0, s>>>(A, B, B2, C, static_cast<int>(M), static_cast<int>(N),
                                                  static_cast<int>(K), ep);
   BF_CUDA(cudaGetLastError());
@@ -239,7 +373,7 @@ KernelSpec simt_gemm_spec(int epi) {
                                 : reinterpret_cast<const void*>(&simt::gemm_f32_kernel<simt::kPlain>);
   k.threads = simt::THREADS;
   k.tile_m = simt::BM;
-  k.tile_n = simt::BN;
+  k.tile_n = epi == simt::kSwiGLU ? simt::Shape<simt::kSwiGLU>::BN : simt::Shape<simt::kPlain>::BN;
   k.tile_k = simt::BK;
   k.stages = 1;
   k.tensor = false;

@@ -12,7 +12,7 @@ inp = make_inputs(wl, 0, 1, torch.device("cuda", 0))
 if wl["kind"] == "attn":
     out = torch.empty_like(inp["Q"])
 else:
-    out = torch.empty(inp["rows"], wl["N"], dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(inp["rows"], wl["N"], dtype=inp["X"].dtype, device="cuda")
 fn = step_fn(wl, inp, sched, out)
 for _ in range(n):
     fn()

@@ -76,3 +76,23 @@ def test_two_rank_row_sharding_gloo():
     for rank, err, t in res:
         assert err == 0.0  # row sharding is exact: rows are independent
         assert t == float(world)  # max over ranks of (1 + rank)
+
+
+def test_c_abi_shard_range_matches_python_shards():
+    """bf_shard_range (the C-ABI's sharding, no GPU needed) equals launcher.shard with 128-row
+    alignment for rows and whole heads for attention; shards tile [0, units) in order."""
+    from paper_2505_07829_b200 import launcher
+
+    for units, world in [(8192, 8), (32768, 8), (1000, 3), (130, 4), (65536, 2), (5, 8)]:
+        prev = 0
+        for r in range(world):
+            a, b = launcher.shard_range("rms_ffn_swiglu", units, world, r)
+            s = launcher.shard(units, r, world, 128)
+            assert (a, b) == (s.start, s.stop)
+            assert a == prev
+            prev = b
+        assert prev == units
+    for heads, world in [(256, 8), (7, 3)]:
+        got = [launcher.shard_range("attention", heads, world, r) for r in range(world)]
+        assert got == [(launcher.shard(heads, r, world).start, launcher.shard(heads, r, world).stop)
+                       for r in range(world)]

@@ -188,13 +188,19 @@ int cmd_run(const Args& a) {
   const int repeat = std::max(1, std::stoi(a.get("repeat", "1")));
   const auto inputs = random_inputs(input_specs(g, b), seed);
   std::map<std::string, Matrix> out;
-  double best_ms = 1e30;
+  double best_ms = 1e30, sum_ms = 0;
+  bfgpu::ExecTiming best_tm;
   for (int r = 0; r < repeat; ++r) {
     const auto t0 = std::chrono::steady_clock::now();
     out = bfgpu::execute(g, inputs, b, cfg);
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    best_ms = std::min(best_ms, ms);
+    if (r > 0 || repeat == 1) sum_ms += ms;
+    if (ms < best_ms) {
+      best_ms = ms;
+      best_tm = bfgpu::last_timing();
+    }
   }
+  const double mean_ms = sum_ms / std::max(1, repeat > 1 ? repeat - 1 : 1);
   for (const auto& [name, m] : out) {
     double sum = 0, sumsq = 0;
     for (Eigen::Index i = 0; i < m.rows(); ++i)
@@ -202,9 +208,13 @@ int cmd_run(const Args& a) {
         sum += m(i, j);
         sumsq += m(i, j) * m(i, j);
       }
-    std::printf("{\"output\": \"%s\", \"rows\": %ld, \"cols\": %ld, \"sum\": %.9g, \"rms\": %.9g, \"ms\": %.3f}\n",
+    std::printf("{\"output\": \"%s\", \"rows\": %ld, \"cols\": %ld, \"sum\": %.9g, \"rms\": %.9g, \"ms\": %.3f, "
+                "\"ms_mean\": %.3f, \"repeat\": %d, \"stages_ms\": {\"convert_in\": %.3f, \"device\": %.3f, "
+                "\"convert_out\": %.3f}, \"h2d_bytes\": %zu, \"d2h_bytes\": %zu}\n",
                 name.c_str(), static_cast<long>(m.rows()), static_cast<long>(m.cols()), sum,
-                std::sqrt(sumsq / std::max<double>(1.0, static_cast<double>(m.rows() * m.cols()))), best_ms);
+                std::sqrt(sumsq / std::max<double>(1.0, static_cast<double>(m.rows() * m.cols()))), best_ms, mean_ms,
+                repeat, best_tm.convert_in_ms, best_tm.device_ms, best_tm.convert_out_ms, best_tm.h2d_bytes,
+                best_tm.d2h_bytes);
   }
   return 0;
 }
