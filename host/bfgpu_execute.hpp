@@ -31,7 +31,7 @@ enum class Precision {
 enum class Route {
   Auto,     // the fused sm_100a kernel if the program is a recognized fused candidate, else Generic
   Fused,    // recognized fused candidates only; anything else throws blockfuse::Error
-  Generic,  // the generic float64 GPU walk (bfgpu_generic.cpp) for any program
+  Generic,  // the block-program compiler (bfgpu_codegen.cpp): generated float64 kernels, any program
 };
 
 struct ExecConfig {
@@ -66,14 +66,20 @@ const ExecTiming& last_timing();
 // Throws blockfuse::Error for anything else.
 Recognized recognize(const blockfuse::BlockGraph& program);
 
-// Any block program on the GPU in float64: the reference's eval_graph/eval_map walk
-// (interpreter.hpp:301-472) with device-resident values and one generic kernel per
-// operator (csrc/generic.cu). Misc nodes call the executors in `opts` on host values.
+// Any block program on the GPU in float64, compiled (host/bfgpu_codegen.cpp): one generated
+// CUDA kernel per top-level operator, NVRTC-compiled for sm_100a and cached, with the
+// numerical-safety pass (row-wise significand/exponent pairs; BFGPU_SAFE=0 disables it).
+// Top-level Misc nodes call the executors in `opts` on host values between kernels.
 std::map<std::string, blockfuse::Matrix> execute_generic(const blockfuse::BlockGraph& program,
                                                          const std::map<std::string, blockfuse::Matrix>& inputs,
                                                          const blockfuse::DimBinding& binding,
                                                          const blockfuse::ExecOptions& opts = {},
                                                          void* stream = nullptr);
+
+// The CUDA source execute_generic generates for `program` at these inputs and binding (up to
+// the first top-level Misc node), without touching a device. For inspection and tests.
+std::string generic_source(const blockfuse::BlockGraph& program, const std::map<std::string, blockfuse::Matrix>& inputs,
+                           const blockfuse::DimBinding& binding);
 
 // Precision from BFGPU_PRECISION (bf16 | f32), default bf16; route from BFGPU_ROUTE
 // (auto | fused | generic), default auto.

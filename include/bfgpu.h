@@ -111,47 +111,25 @@ BF_API int bf_attention(const void* Q, const void* K, const void* Vt, void* O, i
                  int64_t D, int64_t Dv, int dtype, float scale, void* stream);
 
 /* ------------------------------------------------------------------------
- * Generic block-program execution (float64, any program): one kernel per
- * operator kind of the reference IR, driven by the graph walk in
- * host/bfgpu_generic.cpp for programs the fused kernels above do not cover.
- * Replaces: detail::eval_func (interpreter.hpp:263-299) and apply_elementwise
- * (:241-252, scalar_expr.hpp:66-87). Dense row-major float64 device buffers.
+ * Run-time compiled kernels (any block program)
+ *   Programs the fused kernels above do not cover (unfused lower() output,
+ *   partial fusions, other programs) are compiled by the block-program
+ *   compiler of the C++ adapter (host/bfgpu_codegen.cpp): one generated CUDA
+ *   kernel per top-level operator, float64, with the numerical-safety pass
+ *   (row-wise significand/exponent pairs, PAPER.md appendix). These entry
+ *   points compile such source with NVRTC for sm_100a and launch it.
+ * Replaces: the interpretation of eval_graph/eval_map/eval_func
+ *   (interpreter.hpp:263-472): the walk happens once, at compile time.
+ * bf_jit_compile: `source` is CUDA C++ with extern "C" __global__ kernels;
+ *   *module stays valid for the process (cached per device and source text);
+ *   the NVRTC log (warnings or errors) is copied to `log` when given.
+ * bf_jit_launch: args[i] points at the i-th kernel argument (cuLaunchKernel).
  * ---------------------------------------------------------------------- */
-#define BF_GX_ADD 0       /* out = a + b (interpreter.hpp:265-267) */
-#define BF_GX_MUL 1       /* out = a .* b (:268-273) */
-#define BF_GX_ROW_SHIFT 2 /* out(i,j) = m(i,j) + c(i) (:274-279) */
-#define BF_GX_ROW_SCALE 3 /* out(i,j) = m(i,j) * c(i) (:280-287) */
-/* postfix opcodes of bf_gx_elementwise (ScalarExpr::Op, scalar_expr.hpp:18-31;
- * DimTotal is resolved on the host into a CONST) */
-#define BF_GX_EXPR_VAR 0
-#define BF_GX_EXPR_CONST 1
-#define BF_GX_EXPR_ADD 2
-#define BF_GX_EXPR_SUB 3
-#define BF_GX_EXPR_MUL 4
-#define BF_GX_EXPR_DIV 5
-#define BF_GX_EXPR_EXP 6
-#define BF_GX_EXPR_SQRT 7
-#define BF_GX_EXPR_RECIP 8
-#define BF_GX_EXPR_SQUARE 9
-#define BF_GX_EXPR_SIGMOID 10
-BF_API int bf_gx_binary(int op, const double* a, const double* b, double* out, int64_t n, void* stream);
-BF_API int bf_gx_row_op(int op, const double* m, const double* c, double* out, int64_t rows, int64_t cols,
-                        void* stream);
-/* out[i] = sum_j m(i, j)  (row_sum, interpreter.hpp:288) */
-BF_API int bf_gx_row_sum(const double* m, double* out, int64_t rows, int64_t cols, void* stream);
-/* out[M, N] = a[M, K] * b[N, K]^T  (dot, interpreter.hpp:289-294) */
-BF_API int bf_gx_dot(const double* a, const double* b, double* out, int64_t M, int64_t N, int64_t K, void* stream);
-/* out[rows, cols] = u * v^T  (outer, interpreter.hpp:295) */
-BF_API int bf_gx_outer(const double* u, const double* v, double* out, int64_t rows, int64_t cols, void* stream);
-/* out[i] = f(in[i]) for the postfix program (ops, consts) of length len <= 64 */
-BF_API int bf_gx_elementwise(const int8_t* ops, const double* consts, int len, const double* in, double* out,
-                             int64_t n, void* stream);
-/* block moves for split_into_blocks / assemble (interpreter.hpp:76-138): strided
- * device-to-device copy of a rows x cols window (leading dimensions in elements) */
-BF_API int bf_gx_copy2d(double* dst, int64_t dst_ld, const double* src, int64_t src_ld, int64_t rows, int64_t cols,
-                        void* stream);
-/* zero_like (interpreter.hpp:310-316) */
-BF_API int bf_gx_zero(double* out, int64_t n, void* stream);
+BF_API int bf_jit_compile(const char* source, void** module, char* log, size_t log_len);
+/* Compile only (NVRTC to an sm_100a cubin, discarded): needs no device. */
+BF_API int bf_jit_check(const char* source, char* log, size_t log_len);
+BF_API int bf_jit_launch(void* module, const char* kernel, unsigned grid_x, unsigned grid_y, unsigned block,
+                         size_t dyn_smem, void* stream, void** args);
 
 /* ------------------------------------------------------------------------
  * Device memory helpers for host bindings that do not own a CUDA runtime

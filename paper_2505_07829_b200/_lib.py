@@ -52,14 +52,10 @@ _SIGNATURES = [
         ctypes.c_int,
         [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, _vp],
     ),
-    ("bf_gx_binary", ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, _i64, _vp]),
-    ("bf_gx_row_op", ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _vp]),
-    ("bf_gx_row_sum", ctypes.c_int, [_vp, _vp, _i64, _i64, _vp]),
-    ("bf_gx_dot", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
-    ("bf_gx_outer", ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
-    ("bf_gx_elementwise", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp]),
-    ("bf_gx_copy2d", ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
-    ("bf_gx_zero", ctypes.c_int, [_vp, _i64, _vp]),
+    ("bf_jit_compile", ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp), ctypes.c_char_p, ctypes.c_size_t]),
+    ("bf_jit_check", ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
+    ("bf_jit_launch", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
+                                     ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]),
     ("bf_device_alloc", ctypes.c_void_p, [ctypes.c_size_t]),
     ("bf_device_free", ctypes.c_int, [_vp]),
     ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),

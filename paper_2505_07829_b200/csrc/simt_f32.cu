@@ -22,7 +22,11 @@ extern void note_launch();
 
 namespace simt {
 
-constexpr int BM = 64, BK = 16, THREADS = 128;
+// KG warpgroups split each K slice between them (k steps c = g, g + KG, ...), each owning the
+// whole 64 x BN tile; their partial sums meet in SMEM at the end. That keeps the 64 x BN tile
+// (enough CTAs for 1024^2 outputs) and the 8 x 8 register tile (SMEM traffic below the FMA
+// rate) while giving every scheduler KG warps to switch between.
+constexpr int BM = 64, BK = 16, KG = 2, THREADS = 128 * KG;
 constexpr int TM = 8;  // rows per thread (8 thread rows x 8 = 64)
 
 enum Epi : int { kPlain = 0, kSwiGLU = 1, kLNMM = 2 };
@@ -86,19 +90,26 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   using S = Shape<EPI>;
   constexpr int NB = S::NB, BN = S::BN, TN = S::TN;
   constexpr int APAD = BM + 4, BPAD = BN + 4;
-  constexpr int ALOADS = BM * BK / 4 / THREADS;  // float4 loads of A per thread (2)
-  constexpr int BLOADS = BN * BK / 4 / THREADS;  // float4 loads of each B operand per thread
-  __shared__ __align__(16) float As[2][BK][APAD];
-  __shared__ __align__(16) float Bs[2][NB][BK][BPAD];
+  constexpr int RS = THREADS / 4;                // staging rows per pass (4 threads per row, a float4 each)
+  constexpr int ALOADS = BM / RS;                // float4 loads of A per thread
+  constexpr int BLOADS = BN / RS;                // float4 loads of each B operand per thread
+  constexpr int A_FLOATS = 2 * BK * APAD, B_FLOATS = 2 * NB * BK * BPAD;
+  constexpr int PAIRS = NB * TM * TN / 2;        // accumulator pairs per thread
+  static_assert(ALOADS >= 1 && BLOADS >= 1, "staging covers the tile");
+  static_assert(PAIRS / 2 * 128 * 2 <= A_FLOATS + B_FLOATS, "the K-group reduction fits in the staging SMEM");
+  __shared__ __align__(16) float smem[A_FLOATS + B_FLOATS];
   __shared__ float row_a[BM], row_b[BM], col_s[BN];
+  auto As = reinterpret_cast<float (*)[BK][APAD]>(smem);
+  auto Bs = reinterpret_cast<float (*)[NB][BK][BPAD]>(smem + A_FLOATS);
 
   const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
+  const int grp = tid / 128, t128 = tid % 128;
+  const int tx = t128 % 16, ty = t128 / 16;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const bool vec = (K % 4) == 0;
   const float* Bop[2] = {B, B2};
 
-  // staging assignment: rows lr + 32 i of A and of each B operand, K quad kq
+  // staging assignment: rows lr + RS i of A and of each B operand, K quad kq
   const int lr = tid / 4, kq = (tid % 4) * 4;
   // K2: rows are shifted by a pivot (their first element) before the statistics and the
   // contraction: (X - p) Yt^T - (mu - p) colsum(Yt) equals X Yt^T - mu colsum(Yt) without the
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   float piv[ALOADS];
 #pragma unroll
   for (int i = 0; i < ALOADS; ++i) {
-    const int r = m0 + lr + 32 * i;
+    const int r = m0 + lr + RS * i;
     piv[i] = (EPI == kLNMM && r < M) ? __ldg(A + static_cast<size_t>(r) * K) : 0.f;
   }
   float st1[ALOADS] = {}, st2[ALOADS] = {};  // this thread's share of its rows' moments
@@ -116,8 +127,8 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   auto fetch = [&](int k0) {
 #pragma unroll
     for (int i = 0; i < ALOADS; ++i) {
-      ra[i] = load4(A, m0 + lr + 32 * i, M, k0 + kq, K, vec);
-      if (EPI == kLNMM && m0 + lr + 32 * i < M) {
+      ra[i] = load4(A, m0 + lr + RS * i, M, k0 + kq, K, vec);
+      if (EPI == kLNMM && m0 + lr + RS * i < M) {
         // padding lanes past K stay 0 (not -p): only real elements are shifted
         if (k0 + kq + 0 < K) ra[i].x -= piv[i];
         if (k0 + kq + 1 < K) ra[i].y -= piv[i];
@@ -128,12 +139,12 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
 #pragma unroll
     for (int o = 0; o < NB; ++o)
 #pragma unroll
-      for (int i = 0; i < BLOADS; ++i) rb[o][i] = load4(Bop[o], n0 + lr + 32 * i, N, k0 + kq, K, vec);
+      for (int i = 0; i < BLOADS; ++i) rb[o][i] = load4(Bop[o], n0 + lr + RS * i, N, k0 + kq, K, vec);
   };
   auto stash = [&](int buf) {
 #pragma unroll
     for (int i = 0; i < ALOADS; ++i) {
-      const int r = lr + 32 * i;
+      const int r = lr + RS * i;
       As[buf][kq + 0][r] = ra[i].x;
       As[buf][kq + 1][r] = ra[i].y;
       As[buf][kq + 2][r] = ra[i].z;
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     for (int o = 0; o < NB; ++o)
 #pragma unroll
       for (int i = 0; i < BLOADS; ++i) {
-        const int c = lr + 32 * i;
+        const int c = lr + RS * i;
         Bs[buf][o][kq + 0][c] = rb[o][i].x;
         Bs[buf][o][kq + 1][c] = rb[o][i].y;
         Bs[buf][o][kq + 2][c] = rb[o][i].z;
@@ -172,7 +183,8 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     const bool more = k0 + BK < K;
     if (more) fetch(k0 + BK);
 #pragma unroll
-    for (int c = 0; c < BK; ++c) {
+    for (int cc = 0; cc < BK / KG; ++cc) {
+      const int c = cc * KG + grp;
       const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][c][ty * TM]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][c][ty * TM + 4]);
       const unsigned long long a2[TM] = {pack2(a0.x, a0.x), pack2(a0.y, a0.y), pack2(a0.z, a0.z), pack2(a0.w, a0.w),
@@ -197,6 +209,40 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     buf ^= 1;
   }
 
+  // K-group partial sums meet in the (now idle) staging SMEM, half of the pairs at a time
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(smem);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int g = 1; g < KG; ++g) {
+      if (grp == g) {
+        int q = 0;
+#pragma unroll
+        for (int o = 0; o < NB; ++o)
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN / 2; ++j, ++q)
+              if (q / (PAIRS / 2) == h) red[(q % (PAIRS / 2)) * 128 + t128] = acc[o][i][j];
+      }
+      __syncthreads();
+      if (grp == 0) {
+        int q = 0;
+#pragma unroll
+        for (int o = 0; o < NB; ++o)
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN / 2; ++j, ++q)
+              if (q / (PAIRS / 2) == h) {
+                const float2 x = unpack2(acc[o][i][j]), y = unpack2(red[(q % (PAIRS / 2)) * 128 + t128]);
+                acc[o][i][j] = pack2(x.x + y.x, x.y + y.y);
+              }
+      }
+      __syncthreads();
+    }
+  }
+
   if constexpr (EPI != kPlain) {
     // the 4 lanes sharing a row (tid % 4) hold its quarters
 #pragma unroll
@@ -216,7 +262,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     if ((tid & 3) == 0) {
 #pragma unroll
       for (int i = 0; i < ALOADS; ++i) {
-        const int r = lr + 32 * i;
+        const int r = lr + RS * i;
         if constexpr (EPI == kSwiGLU) {
           row_a[r] = 1.0f / sqrtf(st2[i] * ep.inv_k + ep.eps);  // r (rmsnorm scale, lowering.hpp:409-411)
         } else {
@@ -228,11 +274,12 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
       }
       if constexpr (EPI == kLNMM) {
 #pragma unroll
-        for (int i = 0; i < BLOADS; ++i) col_s[lr + 32 * i] = cs[i];
+        for (int i = 0; i < BLOADS; ++i) col_s[lr + RS * i] = cs[i];
       }
     }
     __syncthreads();
   }
+  if (grp != 0) return;
 
 #pragma unroll
   for (int i = 0; i < TM; ++i) {

@@ -2,12 +2,14 @@
 // blockfuse::execute (the reference CPU executor) on the reference's own
 // programs and random_inputs, exposed as C for tests/test_execute_gpu.py.
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <string>
 
 #include "bfgpu_execute.hpp"
 #include "blockfuse/engine.hpp"
 #include "blockfuse/lowering.hpp"
+#include "blockfuse/safe_numerics.hpp"
 
 using namespace blockfuse;
 
@@ -98,6 +100,65 @@ __attribute__((visibility("default"))) int bfx_compare(int which, int snap, cons
       }
     *rel_err = maxd / std::max(maxr, 1e-300);
     *norm_err = maxd / std::max(std::sqrt(ss / static_cast<double>(e.size())), 1e-300);
+    set_msg(msg, msglen, "ok");
+    return 0;
+  } catch (const std::exception& ex) {
+    set_msg(msg, msglen, ex.what());
+    return 1;
+  }
+}
+
+// Attention snapshot `snap` on the compiled (generic) route with Q scaled by `qscale`, so the
+// logits leave exp's range: max rel. error vs safe_attention_rows (safe_numerics.hpp:147)
+// in *err, and the reference interpreter's own error (it overflows) in *ref_err.
+__attribute__((visibility("default"))) int bfx_attention_generic(int snap, const char* binding, double qscale,
+                                                                 double* err, double* ref_err, char* msg,
+                                                                 int msglen) {
+  try {
+    BlockGraph unfused = lower(example(0, 0.0));
+    FuseResult fr = fuse(unfused);
+    const BlockGraph& prog = fr.snapshots.at(snap).program;
+    DimBinding b = parse(binding);
+    auto in = random_inputs(input_specs(unfused, b), 7);
+    in["Q"] = in["Q"] * qscale;
+    bfgpu::ExecConfig cfg;
+    cfg.route = bfgpu::Route::Generic;
+    const Matrix got = bfgpu::execute(prog, in, b, cfg).at("O");
+    const Matrix safe = safe_attention_rows(in.at("Q"), in.at("K"), in.at("Vt"));
+    const Matrix ref = execute(prog, in, b).at("O");
+    auto rel = [&](const Matrix& m) {
+      double d = 0, r = 0;
+      for (long i = 0; i < safe.rows(); ++i)
+        for (long j = 0; j < safe.cols(); ++j) {
+          if (!std::isfinite(m(i, j))) return std::numeric_limits<double>::infinity();
+          d = std::max(d, std::abs(m(i, j) - safe(i, j)));
+          r = std::max(r, std::abs(safe(i, j)));
+        }
+      return d / std::max(r, 1e-300);
+    };
+    *err = rel(got);
+    *ref_err = rel(ref);
+    set_msg(msg, msglen, "ok");
+    return 0;
+  } catch (const std::exception& ex) {
+    set_msg(msg, msglen, ex.what());
+    return 1;
+  }
+}
+
+// The block-program compiler's CUDA source for snapshot `snap` (-2: the unfused lower()
+// program) at `binding` on the reference's random inputs; no device involved.
+__attribute__((visibility("default"))) int bfx_generic_source(int which, int snap, const char* binding, char* out,
+                                                              long outlen, char* msg, int msglen) {
+  try {
+    BlockGraph unfused = lower(example(which, 0.0));
+    FuseResult fr = fuse(unfused);
+    const BlockGraph& prog = snap == -2 ? unfused : (snap == -1 ? fr.snapshots.back().program : fr.snapshots.at(snap).program);
+    DimBinding b = parse(binding);
+    auto in = random_inputs(input_specs(unfused, b), 1);
+    const std::string src = bfgpu::generic_source(prog, in, b);
+    if (static_cast<long>(src.size()) + 1 > outlen) throw Error("source buffer too small");
+    std::memcpy(out, src.c_str(), src.size() + 1);
     set_msg(msg, msglen, "ok");
     return 0;
   } catch (const std::exception& ex) {
