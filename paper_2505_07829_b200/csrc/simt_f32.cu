@@ -26,7 +26,10 @@ namespace simt {
 // whole 64 x BN tile; their partial sums meet in SMEM at the end. That keeps the 64 x BN tile
 // (enough CTAs for 1024^2 outputs) and the 8 x 8 register tile (SMEM traffic below the FMA
 // rate) while giving every scheduler KG warps to switch between.
-constexpr int BM = 64, BK = 16, KG = 2, THREADS = 128 * KG;
+#ifndef BF_SIMT_KG
+#define BF_SIMT_KG 4
+#endif
+constexpr int BM = 64, BK = 16, KG = BF_SIMT_KG, THREADS = 128 * KG;
 constexpr int TM = 8;  // rows per thread (8 thread rows x 8 = 64)
 
 enum Epi : int { kPlain = 0, kSwiGLU = 1, kLNMM = 2 };
@@ -90,7 +93,8 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
   using S = Shape<EPI>;
   constexpr int NB = S::NB, BN = S::BN, TN = S::TN;
   constexpr int APAD = BM + 4, BPAD = BN + 4;
-  constexpr int RS = THREADS / 4;                // staging rows per pass (4 threads per row, a float4 each)
+  constexpr int STAGERS = 256;                   // threads that stage tiles (the first two warpgroups)
+  constexpr int RS = STAGERS / 4;                // staging rows per pass (4 threads per row, a float4 each)
   constexpr int ALOADS = BM / RS;                // float4 loads of A per thread
   constexpr int BLOADS = BN / RS;                // float4 loads of each B operand per thread
   constexpr int A_FLOATS = 2 * BK * APAD, B_FLOATS = 2 * NB * BK * BPAD;
@@ -175,13 +179,16 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
 #pragma unroll
       for (int j = 0; j < TN / 2; ++j) acc[o][i][j] = 0ull;
 
-  fetch(0);
-  stash(0);
+  const bool stager = tid < STAGERS;
+  if (stager) {
+    fetch(0);
+    stash(0);
+  }
   __syncthreads();
   int buf = 0;
   for (int k0 = 0; k0 < K; k0 += BK) {
     const bool more = k0 + BK < K;
-    if (more) fetch(k0 + BK);
+    if (more && stager) fetch(k0 + BK);
 #pragma unroll
     for (int cc = 0; cc < BK / KG; ++cc) {
       const int c = cc * KG + grp;
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
           for (int j = 0; j < TN / 2; ++j) ffma2(acc[o][i][j], a2[i], b2[j]);
       }
     }
-    if (more) stash(buf ^ 1);
+    if (more && stager) stash(buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
     }
   }
 
-  if constexpr (EPI != kPlain) {
+  if (EPI != kPlain && stager) {
     // the 4 lanes sharing a row (tid % 4) hold its quarters
 #pragma unroll
     for (int i = 0; i < ALOADS; ++i) {
@@ -277,8 +284,8 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(const float* __restri
         for (int i = 0; i < BLOADS; ++i) col_s[lr + RS * i] = cs[i];
       }
     }
-    __syncthreads();
   }
+  if (EPI != kPlain) __syncthreads();
   if (grp != 0) return;
 
 #pragma unroll

@@ -108,7 +108,7 @@ L.bfx_attention_generic.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_doub
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, ctypes.c_int]
 got, safe = ctypes.c_double(), ctypes.c_double()
 msg = ctypes.create_string_buffer(1024)
-rc = L.bfx_attention_generic(1, b"M=2x4,N=3x4,D=2x4,L=2x4", 60.0, ctypes.byref(got), ctypes.byref(safe), msg, 1024)
+rc = L.bfx_attention_generic(1, b"M=2x4,N=3x4,D=2x4,L=2x4", 400.0, ctypes.byref(got), ctypes.byref(safe), msg, 1024)
 print(rc, got.value, safe.value, msg.value.decode())
 """
     for env, finite in [("1", True), ("0", False)]:
