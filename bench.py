@@ -259,8 +259,8 @@ def step_fn(wl, inp, schedule, out):
     if kind == "ffn":
         return lambda: ops.rms_ffn_swiglu(inp["X"], inp["Wt"], inp["Vt"], inp["Ut"], schedule=schedule, out=out)
     if kind == "lnmm":
-        return lambda: ops.layernorm_matmul(inp["X"], inp["Yt"], out=out)
-    return lambda: ops.attention(inp["Q"], inp["K"], inp["Vt"], out=out)
+        return lambda: ops.layernorm_matmul(inp["X"], inp["Yt"], out=out, schedule=schedule)
+    return lambda: ops.attention(inp["Q"], inp["K"], inp["Vt"], out=out, schedule=schedule)
 
 
 def check_output(wl, inp, out) -> dict:
@@ -493,7 +493,7 @@ def e2e_adapter(wl: dict, rows: int, precision: str, schedule: str) -> dict:
         with tempfile.TemporaryDirectory() as d:
             r = subprocess.run([str(cli), "snapshots", ex, "--out-dir", d], capture_output=True, text=True, timeout=120)
             n = json.loads(r.stdout)["snapshots"]
-            snap = 1 if (kind == "ffn" and schedule == "two_phase") else n
+            snap = 1 if schedule == "two_phase" else n
             cmd = [str(cli), "run", f"{d}/snapshot_{snap}.json", "--dims", dims, "--block", "128x128", "--repeat", "4",
                    "--precision", precision, "--route", "fused"]
             r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
@@ -599,7 +599,7 @@ def run_ours(args, wl):
     h2d = sum(host[n].numel() * host[n].element_size() for n in names)
     d2h = out_host.numel() * out_host.element_size()
     efn = {"ffn": ops.rms_ffn_swiglu, "lnmm": ops.layernorm_matmul, "attn": ops.attention}[kind]
-    kw = {"schedule": args.schedule} if kind == "ffn" else {}
+    kw = {"schedule": args.schedule}
     e2e_chunks = 1 if f32 else 4
 
     def e2e_step():
@@ -626,7 +626,7 @@ def run_ours(args, wl):
                 "lnmm": lambda: (inp["rows"], wl["K"], wl["N"]),
                 "attn": lambda: (inp["rows"], wl["S"], wl["S"], wl["Dh"], wl["Dh"])}[kind]()
         plan = ops.plan(pattern, dims, dtype=inp["X" if kind != "attn" else "Q"].dtype,
-                        schedule=args.schedule if kind == "ffn" else "fused", device=dev)
+                        schedule=args.schedule, device=dev)
     except Exception as e:  # noqa: BLE001 - reported, not fatal
         plan = {"error": str(e)}
 
@@ -650,6 +650,8 @@ def run_ours(args, wl):
         kkey = plan.get("kernel", KERNELS[kind]) if isinstance(plan, dict) else KERNELS[kind]
         capture = {"ffn": "prof_ffn" if args.schedule == "fused" else "prof_ffn2p", "lnmm": "prof_lnmm",
                    "attn": "prof_attn"}[kind]
+        if args.schedule != "fused" and kind != "ffn":
+            capture = None  # no ncu capture of the staged K2/K3 plans
         if args.workload == "ffn_70b":
             capture = "prof_ffn70b"  # the C3 capture does not describe the 70B shape
         elif args.workload == "lnmm_c1":
@@ -690,7 +692,7 @@ def run_ours(args, wl):
             "data": "synthetic: N(0,1) activations, N(0,1)/sqrt(fan_in) weights, seeded per rank",
             "config": {
                 "workload": wl["name"] + (f" [rows/heads per GPU overridden: {args.rows}]" if args.rows else ""),
-                "schedule": args.schedule if kind == "ffn" else "fused",
+                "schedule": args.schedule,
                 ("heads_per_gpu" if kind == "attn" else "rows_per_gpu"): inp["rows"],
                 "parallelism": f"{'head' if kind == 'attn' else 'row'}-sharded x{world}, no data-path collective",
                 "l2": l2_note,

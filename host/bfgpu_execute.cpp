@@ -415,7 +415,9 @@ std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const st
       out = st.scratch("O", static_cast<size_t>(M * N) * eb);
       const size_t wsb = bf_layernorm_matmul_workspace_bytes(M, K, N, dt);
       void* ws = st.scratch("ws", wsb);
-      check(bf_layernorm_matmul(X, Yt, out, M, K, N, dt, 0.0f, ws, wsb, s), "bf_layernorm_matmul");
+      // snapshot 0 computes the statistics in their own map first (a distinct launch plan)
+      const int sched = rec.snapshot == 0 ? BF_SCHED_STAGED : BF_SCHED_FUSED;
+      check(bf_layernorm_matmul_sched(X, Yt, out, M, K, N, dt, 0.0f, sched, ws, wsb, s), "bf_layernorm_matmul");
       break;
     }
     case Pattern::Attention: {
@@ -427,7 +429,14 @@ std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const st
       out_rows = M;
       out_cols = L;
       out = st.scratch("O", static_cast<size_t>(M * L) * eb);
-      check(bf_attention(Q, K, Vt, out, 1, M, N, D, L, dt, 0.0f, s), "bf_attention");  // scale 1/sqrt(total(D))
+      // snapshot 0 buffers P (T1) between its two maps: the staged plan (bf16); fp32 mode runs the
+      // fused kernel for both snapshots
+      const int sched =
+          rec.materializes_intermediate && cfg.precision == Precision::BF16 ? BF_SCHED_STAGED : BF_SCHED_FUSED;
+      const size_t wsb = bf_attention_workspace_bytes(1, M, N, D, L, dt, sched);
+      void* ws = wsb ? st.scratch("ws", wsb) : nullptr;
+      check(bf_attention_sched(Q, K, Vt, out, 1, M, N, D, L, dt, 0.0f, sched, ws, wsb, s),
+            "bf_attention");  // scale 1/sqrt(total(D))
       break;
     }
   }

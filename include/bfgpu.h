@@ -59,16 +59,25 @@ extern "C" {
 #define BF_DTYPE_BF16 0
 #define BF_DTYPE_F32 1
 
-/* K1 schedules. FUSED runs the whole program in one persistent kernel (final
- * snapshot of fuse(lower(rms_ffn_swiglu()))): gate/up tiles hand H to the
- * down tiles of the same m-unit inside the launch, through a workspace slab
- * that the planner sizes per scheduling group to fit L2. H is not re-read
- * from HBM by a second launch, but at d=4096 and above the slabs of the two
- * groups in flight exceed L2, so part of H is written back (K1 DRAM
- * floor). TWO_PHASE is the reference's first fusion snapshot (one internal
- * buffered edge: H materialized in HBM between two launches). */
-#define BF_FFN_FUSED 0
-#define BF_FFN_TWO_PHASE 1
+/* Schedules: which fusion snapshot of the program a launch executes.
+ *   BF_SCHED_FUSED   the final snapshot of fuse(lower(examples::X())) (engine.hpp:164):
+ *                    one launch, no internal buffered edge.
+ *   BF_SCHED_STAGED  the first snapshot the driver emits, as its own plan:
+ *                    K1  H materialized in HBM between a gate/up and a down launch;
+ *                    K2  the row-statistics map (forall m: for k: sum x, sum x^2) as its
+ *                        own launch before the GEMM map;
+ *                    K3  P = exp(S) materialized in HBM (internal buffered edge T1) between
+ *                        a scores launch and a P.Vt launch.
+ * K1 FUSED: gate/up tiles hand H to the down tiles of the same m-unit inside
+ * the launch, through a workspace slab that the planner sizes per scheduling
+ * group. H is never re-read by a second launch, and its reads are mostly L2
+ * hits, but the TMA-stored H lines do reach HBM: ncu shows DRAM writes = O + H
+ * at every group size tried, including with evict-last stores and
+ * discard.global.L2 after the last reader (profiles/r02_k1_h_writeback.txt). */
+#define BF_SCHED_FUSED 0
+#define BF_SCHED_STAGED 1
+#define BF_FFN_FUSED BF_SCHED_FUSED
+#define BF_FFN_TWO_PHASE BF_SCHED_STAGED
 
 /* ------------------------------------------------------------------------
  * K1  Flash-RMSNorm + FFN-SwiGLU
@@ -97,6 +106,10 @@ BF_API int bf_rms_ffn_swiglu(const void* X, const void* Wt, const void* Vt, cons
 BF_API size_t bf_layernorm_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype);
 BF_API int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, int dtype, float eps,
                         void* workspace, size_t workspace_bytes, void* stream);
+/* Same, for either snapshot (BF_SCHED_FUSED = bf_layernorm_matmul; BF_SCHED_STAGED =
+ * snapshot 1 of the driver, statistics map first, lowering.hpp:573-581). Same workspace. */
+BF_API int bf_layernorm_matmul_sched(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, int dtype,
+                                     float eps, int schedule, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * K3  Rediscovered FlashAttention (non-causal, no mask), online softmax
@@ -109,6 +122,14 @@ BF_API int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M
  * ---------------------------------------------------------------------- */
 BF_API int bf_attention(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
                  int64_t D, int64_t Dv, int dtype, float scale, void* stream);
+/* Either snapshot. BF_SCHED_FUSED needs no workspace (bf_attention). BF_SCHED_STAGED is the
+ * first snapshot (P = T1 buffered; bf16 only): the workspace holds P [BH, Sq, Skv] bf16, the
+ * per-(row, key block) exponent bases and 1/l, and must be 16-byte aligned. */
+BF_API size_t bf_attention_workspace_bytes(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype,
+                                           int schedule);
+BF_API int bf_attention_sched(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq,
+                              int64_t Skv, int64_t D, int64_t Dv, int dtype, float scale, int schedule, void* workspace,
+                              size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * Run-time compiled kernels (any block program)

@@ -23,8 +23,10 @@ BF_ERR_INTERNAL = 4
 BF_DTYPE_BF16 = 0
 BF_DTYPE_F32 = 1
 
-BF_FFN_FUSED = 0
-BF_FFN_TWO_PHASE = 1
+BF_SCHED_FUSED = 0
+BF_SCHED_STAGED = 1
+BF_FFN_FUSED = BF_SCHED_FUSED
+BF_FFN_TWO_PHASE = BF_SCHED_STAGED
 
 BF_PATTERN_RMS_FFN_SWIGLU = 0
 BF_PATTERN_LAYERNORM_MATMUL = 1
@@ -48,9 +50,21 @@ _SIGNATURES = [
         [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, _vp, ctypes.c_size_t, _vp],
     ),
     (
+        "bf_layernorm_matmul_sched",
+        ctypes.c_int,
+        [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, ctypes.c_int, _vp, ctypes.c_size_t, _vp],
+    ),
+    (
         "bf_attention",
         ctypes.c_int,
         [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, _vp],
+    ),
+    ("bf_attention_workspace_bytes", ctypes.c_size_t, [_i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int]),
+    (
+        "bf_attention_sched",
+        ctypes.c_int,
+        [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_float, ctypes.c_int, _vp,
+         ctypes.c_size_t, _vp],
     ),
     ("bf_jit_compile", ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp), ctypes.c_char_p, ctypes.c_size_t]),
     ("bf_jit_check", ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),

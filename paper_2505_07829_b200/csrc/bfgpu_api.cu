@@ -58,13 +58,14 @@ void ffn_swiglu_f32(const void* X, const void* Wt, const void* Vt, const void* U
 size_t ffn_f32_workspace_bytes(int64_t M, int64_t F);
 
 size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype);
-void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
-               size_t ws_bytes, cudaStream_t stream);
+void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, int schedule,
+               void* ws, size_t ws_bytes, cudaStream_t stream);
 void lnmm_f32(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
               size_t ws_bytes, cudaStream_t stream);
 
 void attention_bf16(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
-                    int64_t D, int64_t Dv, float scale, cudaStream_t stream);
+                    int64_t D, int64_t Dv, float scale, int schedule, void* ws, size_t ws_bytes, cudaStream_t stream);
+size_t attention_staged_workspace_bytes(int64_t BH, int64_t Sq, int64_t Skv);
 void attention_f32(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
                    int64_t D, int64_t Dv, float scale, cudaStream_t stream);
 
@@ -119,14 +120,20 @@ size_t bf_layernorm_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N, int 
 
 int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, int dtype, float eps,
                         void* workspace, size_t workspace_bytes, void* stream) {
+  return bf_layernorm_matmul_sched(X, Yt, O, M, K, N, dtype, eps, BF_SCHED_FUSED, workspace, workspace_bytes, stream);
+}
+
+int bf_layernorm_matmul_sched(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, int dtype,
+                              float eps, int schedule, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
+    BF_CHECK_ARG(schedule == BF_SCHED_FUSED || schedule == BF_SCHED_STAGED, "bf_layernorm_matmul: bad schedule");
     BF_CHECK_ARG(X && Yt && O, "bf_layernorm_matmul: null pointer");
     BF_CHECK_ARG(dtype != BF_DTYPE_BF16 || (aligned16(X) && aligned16(Yt) && aligned16(O) && aligned16(workspace)),
                  "bf_layernorm_matmul: bf16 buffers must be 16-byte aligned");
     require_sm100();
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == BF_DTYPE_BF16)
-      lnmm_bf16(X, Yt, O, M, K, N, eps, workspace, workspace_bytes, s);
+      lnmm_bf16(X, Yt, O, M, K, N, eps, schedule, workspace, workspace_bytes, s);
     else if (dtype == BF_DTYPE_F32)
       lnmm_f32(X, Yt, O, M, K, N, eps, workspace, workspace_bytes, s);
     else
@@ -136,14 +143,31 @@ int bf_layernorm_matmul(const void* X, const void* Yt, void* O, int64_t M, int64
 
 int bf_attention(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
                  int64_t D, int64_t Dv, int dtype, float scale, void* stream) {
+  return bf_attention_sched(Q, K, Vt, O, BH, Sq, Skv, D, Dv, dtype, scale, BF_SCHED_FUSED, nullptr, 0, stream);
+}
+
+size_t bf_attention_workspace_bytes(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype,
+                                    int schedule) {
+  (void)D;
+  (void)Dv;
+  if (BH <= 0 || Sq <= 0 || Skv <= 0 || schedule != BF_SCHED_STAGED || dtype != BF_DTYPE_BF16) return 0;
+  return attention_staged_workspace_bytes(BH, Sq, Skv);
+}
+
+int bf_attention_sched(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
+                       int64_t D, int64_t Dv, int dtype, float scale, int schedule, void* workspace,
+                       size_t workspace_bytes, void* stream) {
   return guarded([&] {
+    BF_CHECK_ARG(schedule == BF_SCHED_FUSED || schedule == BF_SCHED_STAGED, "bf_attention: bad schedule");
+    BF_CHECK_ARG(schedule == BF_SCHED_FUSED || dtype == BF_DTYPE_BF16,
+                 "bf_attention: the staged (P-buffered) schedule is bf16 only");
     BF_CHECK_ARG(Q && K && Vt && O, "bf_attention: null pointer");
     BF_CHECK_ARG(dtype != BF_DTYPE_BF16 || (aligned16(Q) && aligned16(K) && aligned16(Vt) && aligned16(O)),
                  "bf_attention: bf16 buffers must be 16-byte aligned");
     require_sm100();
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == BF_DTYPE_BF16)
-      attention_bf16(Q, K, Vt, O, BH, Sq, Skv, D, Dv, scale, s);
+      attention_bf16(Q, K, Vt, O, BH, Sq, Skv, D, Dv, scale, schedule, workspace, workspace_bytes, s);
     else if (dtype == BF_DTYPE_F32)
       attention_f32(Q, K, Vt, O, BH, Sq, Skv, D, Dv, scale, s);
     else

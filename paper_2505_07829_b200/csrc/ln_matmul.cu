@@ -355,15 +355,15 @@ size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype) {
   return std::max(align_up(static_cast<size_t>(N) * 4, 256) + 256, lnmm2_workspace_bytes(M, N));
 }
 
-void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
-               size_t ws_bytes, cudaStream_t stream) {
+void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, int schedule,
+               void* ws, size_t ws_bytes, cudaStream_t stream) {
   using namespace lnmm;
   BF_CHECK_ARG(M > 0 && K > 0 && N > 0, "bf_layernorm_matmul: sizes must be positive");
   BF_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "bf_layernorm_matmul: K and N must be multiples of 8");
   BF_CHECK_ARG(M < (1ll << 31) && K < (1ll << 31) && N < (1ll << 31), "bf_layernorm_matmul: dimension too large");
   BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm_workspace_bytes(M, K, N, BF_DTYPE_BF16),
                "bf_layernorm_matmul: workspace too small");
-  const Plan pl = plan_lnmm(M, K, N, BF_DTYPE_BF16);
+  const Plan pl = plan_lnmm(M, K, N, BF_DTYPE_BF16, schedule);
   if (pl.spec.cluster == 2) {
     lnmm_bf16_2sm(pl, X, Yt, O, eps, ws, ws_bytes, stream);
     return;

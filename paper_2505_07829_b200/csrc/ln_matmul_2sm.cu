@@ -62,7 +62,34 @@ struct Params {
   float* row_rstd;  // [M]
   int* col_ready;   // CTAs that published their colsum slice
   int* row_ready;   // [2*Mt] per 128-row tile: 1 once its statistics are published
+  int staged;       // snapshot-0 schedule: statistics were computed by lnmm_stats_kernel before
+                    // this launch (the program's separate `for k` map over X), nothing to wait for
 };
+
+// Snapshot 0 of fuse(lower(layernorm_matmul())) computes the row statistics in their own map
+// (forall m: for k: t1 += row_sum(X), t2 += row_sum(square(X))) before the forall-n GEMM map,
+// and colsum(Yt) inside it. As a launch: one warp per row of X, then per row of Yt.
+__global__ void __launch_bounds__(256) lnmm_stats_kernel(const Params p) {
+  using namespace dev;
+  const uint32_t lane = lane_id();
+  const int warps = static_cast<int>(gridDim.x * blockDim.x / 32);
+  for (int r = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) / 32); r < p.M + p.N; r += warps) {
+    if (r < p.M) {
+      const __nv_bfloat16* rows[1] = {p.X + static_cast<size_t>(r) * p.K};
+      float t1[1], t2[1], piv[1];
+      warp_rows_moments_bf16<1, true>(rows, p.K, lane, t1, t2, piv);
+      if (lane == 0) {
+        const float dm = t1[0] * p.inv_k;
+        p.row_mu[r] = -(piv[0] + dm);
+        p.row_rstd[r] = 1.0f / sqrtf(t2[0] * p.inv_k - dm * dm + p.eps);
+      }
+    } else {
+      const int n = r - p.M;
+      const float2 mom = warp_row_moments_bf16(p.Yt + static_cast<size_t>(n) * p.K, p.K, lane);
+      if (lane == 0) p.colsum[n] = mom.x;
+    }
+  }
+}
 
 __device__ __forceinline__ void decode(const Params& p, int t, int& m, int& n) {
   // Within a group of m-units, n is the slow index: every (m, 0) tile precedes (m, n>0).
@@ -180,7 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
 
     // ---- t4 = colsum(Yt): this CTA's slice, one warp per Yt row
-    {
+    if (!p.staged) {
       const int per = (p.N + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
       const int n0 = static_cast<int>(blockIdx.x) * per, n1 = min(p.N, n0 + per);
       for (int n = n0 + static_cast<int>(q); n < n1; n += 4) {
@@ -236,8 +263,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int row0 = mtile * BM;
       // ---- t1, t2 of this CTA's rows are produced by the CTA that owns the m-unit's
       // first n-tile (see header); in the first wave nobody ran ahead, so do it now.
-      if (t == cluster_id && n == 0 && mtile < num_rt) compute_row_tile(mtile);
-      if (store_leader) {
+      if (!p.staged && t == cluster_id && n == 0 && mtile < num_rt) compute_row_tile(mtile);
+      if (store_leader && !p.staged) {
         const uint64_t t0 = globaltimer_ns();
         while ((!col_seen && ld_acquire_gpu(p.col_ready) < static_cast<int>(gridDim.x)) ||
                (mtile < num_rt && ld_acquire_gpu(&p.row_ready[mtile]) < 1)) {  // no rows: nothing to wait for
@@ -309,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // one mainloop ahead of that tile's X stream, which then finds the rows in L2
       // (X leaves HBM once), and ahead of every other tile of the m-unit.
       const int tn = t + num_clusters;
-      if (tn < p.num_tiles) {
+      if (tn < p.num_tiles && !p.staged) {
         int m2, n2;
         decode(p, tn, m2, n2);
         const int mt2 = m2 * 2 + static_cast<int>(rank);
@@ -386,7 +413,17 @@ void lnmm_bf16_2sm(const Plan& pl, const void* X, const void* Yt, void* O, float
   const CUtensorMap tm_x = make_tmap_bf16(X, M, K, K, BK, BM);
   const CUtensorMap tm_y = make_tmap_bf16(Yt, N, K, K, BK, 128);
   const CUtensorMap tm_o = make_tmap_bf16(O, M, N, N, BK, BM);
-  BF_CUDA(cudaMemsetAsync(p.col_ready, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
+  p.staged = pl.schedule == BF_SCHED_STAGED;
+  if (p.staged) {
+    // the statistics map as its own launch: 8 warps per CTA, a few rows per warp
+    const int64_t warps_needed = (M + N + 3) / 4;
+    const int grid = static_cast<int>(std::min<int64_t>((warps_needed + 7) / 8, static_cast<int64_t>(pl.dev.sms) * 8));
+    lnmm_stats_kernel<<<grid, 256, 0, stream>>>(p);
+    BF_CUDA(cudaGetLastError());
+    note_launch();
+  } else {
+    BF_CUDA(cudaMemsetAsync(p.col_ready, 0, (static_cast<size_t>(p.Mt) * 2 + 1) * sizeof(int), stream));
+  }
   launch_planned(pl, ln_matmul_2sm_kernel, stream, tm_x, tm_y, tm_o, p);
 }
 

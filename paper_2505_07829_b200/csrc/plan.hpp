@@ -80,8 +80,8 @@ void ensure_smem_attr(const void* func, int bytes);
 int resident_ctas(const KernelSpec& k);
 
 const Plan& plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule);
-const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype);
-const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype);
+const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int schedule = 0);
+const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype, int schedule = 0);
 std::string plan_json(const Plan& p);
 
 // Kernel descriptors, defined next to each kernel.
@@ -90,6 +90,7 @@ KernelSpec ffn1_spec();
 KernelSpec lnmm2_spec();
 KernelSpec lnmm1_spec();
 KernelSpec attn_spec(int D, int Dv, int emu);
+KernelSpec attn_staged_spec(int D, int Dv);
 KernelSpec simt_gemm_spec(int epi);
 KernelSpec simt_attn_spec();
 

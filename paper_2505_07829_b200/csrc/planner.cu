@@ -200,10 +200,11 @@ static Plan make_plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype,
 }
 
 // ------------------------------------------------------------------ K2
-static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
+static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int schedule) {
   Plan p;
   p.pattern = kPatLnmm;
   p.dtype = dtype;
+  p.schedule = schedule;
   p.dev = device_info(current_device());
   p.dims[0] = M, p.dims[1] = K, p.dims[2] = N;
   const double eb = dtype == BF_DTYPE_BF16 ? 2.0 : 4.0;
@@ -216,12 +217,13 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
     p.tiles = p.units * cdiv(N, p.spec.tile_n);
     p.resident_ctas = resident_ctas(p.spec);
     p.grid = static_cast<int>(std::min<int64_t>(p.tiles, 1 << 30));
-    why << "fp32 mode: FP32 SIMT FMA, statistics and colsum(Yt) folded into the K loop of each tile";
+    why << "fp32 mode: FP32 SIMT FMA, statistics and colsum(Yt) folded into the K loop of each tile"
+        << (schedule == BF_SCHED_STAGED ? " (the same kernel serves the staged snapshot in fp32)" : "");
     p.notes = why.str();
     check_budgets(p);
     return p;
   }
-  const bool one_sm = env_int("BFGPU_LNMM_1SM", 0) == 1;
+  const bool one_sm = env_int("BFGPU_LNMM_1SM", 0) == 1 && schedule == BF_SCHED_FUSED;
   p.spec = one_sm ? lnmm1_spec() : lnmm2_spec();
   why << (one_sm ? "override BFGPU_LNMM_1SM=1: 1-SM kernel; " : "CTA-pair kernel, 256x256 output tiles; ");
   const int unit = p.spec.tile_m;
@@ -240,8 +242,13 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
   }
   p.group = std::max(1, group);
   p.group_slab_bytes = 2.0 * p.group * unit * K;
-  why << "group " << p.group << " m-units: X slab " << p.group_slab_bytes / 1e6 << " MB; row statistics and "
-      << "colsum(Yt) computed once and published through the workspace (grid-wide flags: cooperative launch)";
+  why << "group " << p.group << " m-units: X slab " << p.group_slab_bytes / 1e6 << " MB; ";
+  if (schedule == BF_SCHED_STAGED)
+    why << "staged (first snapshot): the row-statistics map runs as its own launch (one warp per row of X, "
+           "then of Yt), then the GEMM launch reads mu, rstd and colsum(Yt) from the workspace";
+  else
+    why << "row statistics and colsum(Yt) computed once inside the launch and published through the workspace "
+           "(grid-wide flags: cooperative launch)";
   finish_grid(p, p.tiles);
   p.notes = why.str();
   check_budgets(p);
@@ -249,10 +256,12 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
 }
 
 // ------------------------------------------------------------------ K3
-static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype) {
+static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype,
+                                int schedule) {
   Plan p;
   p.pattern = kPatAttn;
   p.dtype = dtype;
+  p.schedule = schedule;
   p.dev = device_info(current_device());
   p.dims[0] = BH, p.dims[1] = Sq, p.dims[2] = Skv, p.dims[3] = D, p.dims[4] = Dv;
   const double eb = dtype == BF_DTYPE_BF16 ? 2.0 : 4.0;
@@ -267,6 +276,19 @@ static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, 
     p.resident_ctas = resident_ctas(p.spec);
     p.grid = static_cast<int>(std::min<int64_t>(p.tiles, 1 << 30));
     why << "fp32 mode: FP32 SIMT online softmax, one CTA per (head, 16 query rows)";
+    p.notes = why.str();
+    check_budgets(p);
+    return p;
+  }
+  if (schedule == BF_SCHED_STAGED) {
+    p.spec = attn_staged_spec(static_cast<int>(D), static_cast<int>(Dv));
+    p.units = cdiv(Sq, p.spec.tile_m);
+    p.tiles = p.units * BH;
+    if (p.tiles >= (1ll << 31)) throw Status(BF_ERR_INVALID_ARGUMENT, "bf_attention: too many tiles");
+    finish_grid(p, p.tiles);
+    p.group_slab_bytes = 2.0 * BH * static_cast<double>(Sq) * Skv;
+    why << "staged (first snapshot, P buffered): scores launch writes P = exp(S - base) per (head, 128 queries) to "
+           "HBM (" << p.group_slab_bytes / 1e6 << " MB), then a persistent P.Vt GEMM launch with the 1/l row scale";
     p.notes = why.str();
     check_budgets(p);
     return p;
@@ -311,19 +333,20 @@ const Plan& plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int 
                      [&] { return make_plan_ffn(M, D, F, N, dtype, schedule); });
 }
 
-const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype) {
-  return cached_plan(PlanKey{kPatLnmm, M, K, N, 0, 0, dtype, 0, current_device()},
-                     [&] { return make_plan_lnmm(M, K, N, dtype); });
+const Plan& plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int schedule) {
+  return cached_plan(PlanKey{kPatLnmm, M, K, N, 0, 0, dtype, schedule, current_device()},
+                     [&] { return make_plan_lnmm(M, K, N, dtype, schedule); });
 }
 
-const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype) {
-  return cached_plan(PlanKey{kPatAttn, BH, Sq, Skv, D, Dv, dtype, 0, current_device()},
-                     [&] { return make_plan_attention(BH, Sq, Skv, D, Dv, dtype); });
+const Plan& plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, int64_t Dv, int dtype, int schedule) {
+  return cached_plan(PlanKey{kPatAttn, BH, Sq, Skv, D, Dv, dtype, schedule, current_device()},
+                     [&] { return make_plan_attention(BH, Sq, Skv, D, Dv, dtype, schedule); });
 }
 
 std::string plan_json(const Plan& p) {
   static const char* pat[] = {"rms_ffn_swiglu", "layernorm_matmul", "attention"};
   static const char* sync[] = {"none", "segment", "wave"};
+  static const char* sched[] = {"fused", "staged"};
   auto esc = [](const std::string& s) {
     std::string o;
     for (char c : s) {
@@ -334,7 +357,7 @@ std::string plan_json(const Plan& p) {
   };
   std::ostringstream j;
   j << "{\"pattern\": \"" << pat[p.pattern] << "\", \"dtype\": \"" << (p.dtype == BF_DTYPE_BF16 ? "bf16" : "f32")
-    << "\", \"kernel\": \"" << p.spec.name << "\", \"engine\": \"" << (p.spec.tensor ? "tcgen05" : "fp32-simt")
+    << "\", \"schedule\": \"" << sched[p.schedule ? 1 : 0] << "\", \"kernel\": \"" << p.spec.name << "\", \"engine\": \"" << (p.spec.tensor ? "tcgen05" : "fp32-simt")
     << "\", \"dims\": [" << p.dims[0] << ", " << p.dims[1] << ", " << p.dims[2] << ", " << p.dims[3] << ", "
     << p.dims[4] << "], \"tile\": [" << p.spec.tile_m << ", " << p.spec.tile_n << ", " << p.spec.tile_k
     << "], \"cluster\": " << p.spec.cluster << ", \"threads\": " << p.spec.threads << ", \"stages\": "
@@ -364,10 +387,10 @@ extern "C" int bf_plan_json(int pattern, const int64_t* dims, int ndims, int dty
       p = plan_ffn(dims[0], dims[1], dims[2], dims[3], dtype, schedule);
     } else if (pattern == BF_PATTERN_LAYERNORM_MATMUL) {
       BF_CHECK_ARG(ndims == 3, "bf_plan_json: layernorm_matmul takes {M, K, N}");
-      p = plan_lnmm(dims[0], dims[1], dims[2], dtype);
+      p = plan_lnmm(dims[0], dims[1], dims[2], dtype, schedule);
     } else if (pattern == BF_PATTERN_ATTENTION) {
       BF_CHECK_ARG(ndims == 5, "bf_plan_json: attention takes {BH, Sq, Skv, D, Dv}");
-      p = plan_attention(dims[0], dims[1], dims[2], dims[3], dims[4], dtype);
+      p = plan_attention(dims[0], dims[1], dims[2], dims[3], dims[4], dtype, schedule);
     } else {
       throw Status(BF_ERR_INVALID_ARGUMENT, "bf_plan_json: unknown pattern");
     }

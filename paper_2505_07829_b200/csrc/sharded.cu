@@ -138,11 +138,12 @@ int bf_launch_sharded(int pattern, int ngpu, const bf_shard_io* io, const int64_
                                dims[3], dtype, eps_or_scale, schedule, io[g].workspace, io[g].workspace_bytes,
                                io[g].stream);
       else if (pattern == BF_PATTERN_LAYERNORM_MATMUL)
-        rc = bf_layernorm_matmul(io[g].in[0], io[g].in[1], io[g].out, n, dims[1], dims[2], dtype, eps_or_scale,
-                                 io[g].workspace, io[g].workspace_bytes, io[g].stream);
+        rc = bf_layernorm_matmul_sched(io[g].in[0], io[g].in[1], io[g].out, n, dims[1], dims[2], dtype, eps_or_scale,
+                                       schedule, io[g].workspace, io[g].workspace_bytes, io[g].stream);
       else
-        rc = bf_attention(io[g].in[0], io[g].in[1], io[g].in[2], io[g].out, n, dims[1], dims[2], dims[3], dims[4],
-                          dtype, eps_or_scale, io[g].stream);
+        rc = bf_attention_sched(io[g].in[0], io[g].in[1], io[g].in[2], io[g].out, n, dims[1], dims[2], dims[3],
+                                dims[4], dtype, eps_or_scale, schedule, io[g].workspace, io[g].workspace_bytes,
+                                io[g].stream);
       if (rc != BF_OK) throw Status(rc, "shard " + std::to_string(g) + ": " + bf_last_error());
     }
     if (!gather) return;

@@ -9,8 +9,12 @@ from __future__ import annotations
 import torch
 
 from . import _lib
-from ._lib import (BF_DTYPE_BF16, BF_DTYPE_F32, BF_FFN_FUSED, BF_FFN_TWO_PHASE, BF_PATTERN_ATTENTION,
-                   BF_PATTERN_LAYERNORM_MATMUL, BF_PATTERN_RMS_FFN_SWIGLU, check)
+from ._lib import (BF_DTYPE_BF16, BF_DTYPE_F32, BF_PATTERN_ATTENTION, BF_PATTERN_LAYERNORM_MATMUL,
+                   BF_PATTERN_RMS_FFN_SWIGLU, BF_SCHED_FUSED, BF_SCHED_STAGED, check)
+
+# schedule name -> code. "two_phase" (the first fusion snapshot of each program) is the name the
+# K1 API has always used; "staged" is the same thing.
+SCHEDULES = {"fused": BF_SCHED_FUSED, "two_phase": BF_SCHED_STAGED, "staged": BF_SCHED_STAGED}
 
 # one cached workspace per (device, stream): calls on different streams may overlap
 _WS: dict[tuple[int, int], torch.Tensor] = {}
@@ -68,7 +72,7 @@ def rms_ffn_swiglu(X, Wt, Vt, Ut, eps: float = 0.0, schedule: str = "fused", out
     _require(Wt, "Wt", (F, D), dt, dev)
     _require(Vt, "Vt", (F, D), dt, dev)
     _require(Ut, "Ut", (N, F), dt, dev)
-    sched = {"fused": BF_FFN_FUSED, "two_phase": BF_FFN_TWO_PHASE}[schedule]
+    sched = SCHEDULES[schedule]
     if out is None:
         out = torch.empty((M, N), dtype=dt, device=dev)
     _require(out, "out", (M, N), dt, dev)
@@ -86,8 +90,13 @@ def rms_ffn_swiglu(X, Wt, Vt, Ut, eps: float = 0.0, schedule: str = "fused", out
     return out
 
 
-def layernorm_matmul(X, Yt, eps: float = 0.0, out=None, workspace=None):
-    """O = layernorm(X) Yt^T without eps/gamma/beta (ref::layernorm_matmul, interpreter.hpp:549-551)."""
+def layernorm_matmul(X, Yt, eps: float = 0.0, out=None, workspace=None, schedule: str = "fused"):
+    """O = layernorm(X) Yt^T without eps/gamma/beta (ref::layernorm_matmul, interpreter.hpp:549-551).
+
+    schedule "fused": the final fusion snapshot (statistics inside the GEMM launch); "staged":
+    the first snapshot (the row-statistics map as its own launch, then the GEMM map).
+    """
+    sched = SCHEDULES[schedule]
     M, K = X.shape
     N = Yt.shape[0]
     dt = X.dtype
@@ -103,19 +112,22 @@ def layernorm_matmul(X, Yt, eps: float = 0.0, out=None, workspace=None):
     with torch.cuda.device(dev):
         ws = workspace if workspace is not None else _workspace(nbytes, dev)
         check(
-            L.bf_layernorm_matmul(
-                X.data_ptr(), Yt.data_ptr(), out.data_ptr(), M, K, N, code, float(eps), ws.data_ptr(), ws.numel(),
-                _stream_ptr(dev),
+            L.bf_layernorm_matmul_sched(
+                X.data_ptr(), Yt.data_ptr(), out.data_ptr(), M, K, N, code, float(eps), sched, ws.data_ptr(),
+                ws.numel(), _stream_ptr(dev),
             )
         )
     return out
 
 
-def attention(Q, K, Vt, scale: float | None = None, out=None):
+def attention(Q, K, Vt, scale: float | None = None, out=None, schedule: str = "fused", workspace=None):
     """O = softmax(scale Q K^T) V with V given as Vt (ref::attention, interpreter.hpp:543-547).
 
     Q: [..., Sq, D], K: [..., Skv, D], Vt: [..., Dv, Skv]; leading dims are heads.
+    schedule "fused": the final snapshot (online softmax, P never leaves the chip); "staged":
+    the first snapshot (P = exp(S) buffered in an HBM workspace between two launches; bf16).
     """
+    sched = SCHEDULES[schedule]
     *lead, Sq, D = Q.shape
     Skv = K.shape[-2]
     Dv = Vt.shape[-2]
@@ -131,11 +143,17 @@ def attention(Q, K, Vt, scale: float | None = None, out=None):
         out = torch.empty((*lead, Sq, Dv), dtype=dt, device=dev)
     _require(out, "out", (*lead, Sq, Dv), dt, dev)
     L = _lib.lib()
+    code = _dtype_code(Q)
+    nbytes = L.bf_attention_workspace_bytes(BH, Sq, Skv, D, Dv, code, sched)
     with torch.cuda.device(dev):
+        ws_ptr, ws_len = 0, 0
+        if nbytes:
+            ws = workspace if workspace is not None else _workspace(nbytes, dev)
+            ws_ptr, ws_len = ws.data_ptr(), ws.numel()
         check(
-            L.bf_attention(
-                Q.data_ptr(), K.data_ptr(), Vt.data_ptr(), out.data_ptr(), BH, Sq, Skv, D, Dv, _dtype_code(Q),
-                float(scale) if scale is not None else 0.0, _stream_ptr(dev),
+            L.bf_attention_sched(
+                Q.data_ptr(), K.data_ptr(), Vt.data_ptr(), out.data_ptr(), BH, Sq, Skv, D, Dv, code,
+                float(scale) if scale is not None else 0.0, sched, ws_ptr, ws_len, _stream_ptr(dev),
             )
         )
     return out
@@ -159,7 +177,7 @@ def plan(pattern: str, dims, dtype=torch.bfloat16, schedule: str = "fused", devi
     arr = (ctypes.c_int64 * len(dims))(*[int(d) for d in dims])
     buf = ctypes.create_string_buffer(8192)
     code = BF_DTYPE_BF16 if dtype == torch.bfloat16 else BF_DTYPE_F32
-    sched = {"fused": BF_FFN_FUSED, "two_phase": BF_FFN_TWO_PHASE}[schedule]
+    sched = SCHEDULES[schedule]
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     with torch.cuda.device(dev):
         check(_lib.lib().bf_plan_json(pid, arr, len(dims), code, sched, buf, len(buf)))

@@ -135,9 +135,27 @@ t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
 O = ops.rms_ffn_swiglu(t(X[s.start:s.stop]), t(Wt), t(Vt), t(Ut))
 torch.cuda.synchronize()
 full = gather_rows(O.float().cpu(), shards)   # gloo all-gather of the row shards
+# K2: token rows, Yt replicated
+Mx, K2, N2 = 700, 256, 384
+Xl = bf16_round(rng.standard_normal((Mx, K2)) * 2 + 1); Yt = bf16_round(rng.standard_normal((N2, K2)))
+lsh = [shard(Mx, r, 2, 128) for r in range(2)]
+Ol = ops.layernorm_matmul(t(Xl[lsh[rank].start:lsh[rank].stop]), t(Yt))
+torch.cuda.synchronize()
+full_l = gather_rows(Ol.float().cpu(), lsh)
+# K3: heads
+BH, S, Dh = 5, 256, 128
+Q = bf16_round(rng.standard_normal((BH, S, Dh))); Kk = bf16_round(rng.standard_normal((BH, S, Dh)))
+Va = bf16_round(rng.standard_normal((BH, Dh, S)))
+hsh = [shard(BH, r, 2, 1) for r in range(2)]
+h = hsh[rank]
+Oa = ops.attention(t(Q[h.start:h.stop]), t(Kk[h.start:h.stop]), t(Va[h.start:h.stop]))
+torch.cuda.synchronize()
+full_a = gather_rows(Oa.float().cpu(), hsh)
 if rank == 0:
     from oracle import cpu
     assert_bf16_close(full.double().numpy(), cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 2-rank gather vs oracle")
+    assert_bf16_close(full_l.double().numpy(), cpu.layernorm_matmul(Xl, Yt), "K2 2-rank gather vs oracle")
+    assert_bf16_close(full_a.double().numpy(), cpu.attention_safe(Q, Kk, Va), "K3 2-rank head gather vs oracle")
     print("ok", full.shape)
 dist.barrier()
 dist.destroy_process_group()
@@ -145,8 +163,8 @@ dist.destroy_process_group()
 
 
 def test_two_process_row_shards_gloo():
-    """World size 2, one process per shard (both on cuda:0 here), each running the K1 kernel on its
-    rows; the gathered output matches the oracle."""
+    """World size 2, one process per shard (both on cuda:0 here), each running K1 and K2 on its
+    rows and K3 on its heads; the gathered outputs match the oracle."""
     import socket
 
     with socket.socket() as so:
