@@ -349,9 +349,10 @@ size_t lnmm2_workspace_bytes(int64_t M, int64_t N);
 void lnmm_bf16_2sm(const Plan& pl, const void* X, const void* Yt, void* O, float eps, void* ws, size_t ws_bytes,
                    cudaStream_t stream);
 
+size_t lnmm_f32x3_workspace_bytes(int64_t M, int64_t K, int64_t N);
+
 size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype) {
-  (void)K;
-  if (dtype != BF_DTYPE_BF16) return 256;
+  if (dtype != BF_DTYPE_BF16) return lnmm_f32x3_workspace_bytes(M, K, N);  // the 3xTF32 operands
   return std::max(align_up(static_cast<size_t>(N) * 4, 256) + 256, lnmm2_workspace_bytes(M, N));
 }
 

@@ -92,6 +92,7 @@ KernelSpec lnmm1_spec();
 KernelSpec attn_spec(int D, int Dv, int emu);
 KernelSpec attn_staged_spec(int D, int Dv);
 KernelSpec simt_gemm_spec(int epi);
+KernelSpec f32x3_gemm_spec();
 KernelSpec simt_attn_spec();
 
 extern void note_launch();

@@ -460,11 +460,17 @@ void ffn_swiglu_f32(const void* X, const void* Wt, const void* Vt, const void* U
                                   {0.f, 0.f}, stream);
 }
 
+void lnmm_f32x3(const Plan& pl, const void* X, const void* Yt, void* O, float eps, void* ws, size_t ws_bytes,
+                cudaStream_t stream);
+
 void lnmm_f32(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, void* ws,
               size_t ws_bytes, cudaStream_t stream) {
-  (void)ws;
-  (void)ws_bytes;
   BF_CHECK_ARG(M > 0 && K > 0 && N > 0, "bf_layernorm_matmul: sizes must be positive");
+  const Plan& pl = plan_lnmm(M, K, N, BF_DTYPE_F32);
+  if (pl.spec.tensor) {
+    lnmm_f32x3(pl, X, Yt, O, eps, ws, ws_bytes, stream);
+    return;
+  }
   simt::launch_gemm<simt::kLNMM>(static_cast<const float*>(X), static_cast<const float*>(Yt), nullptr,
                                  static_cast<float*>(O), M, N, K, {1.0f / static_cast<float>(K), eps}, stream);
 }
