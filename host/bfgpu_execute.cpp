@@ -160,41 +160,35 @@ void parallel_rows(long n, long grain, Fn fn) {
   for (auto& th : pool) th.join();
 }
 
-// Column-major Eigen storage -> row-major device layout (bf16 or fp32), 32x32 tiles, row
-// bands in parallel. `dst` is page-locked so the copy that follows is asynchronous.
-void to_device_layout(const Matrix& m, Precision prec, void* dst) {
-  const long R = m.rows(), C = m.cols();
+// Column-major Eigen storage -> the same storage order in bf16/fp32 (a contiguous pass, split
+// across the host threads). `dst` is page-locked so the copy that follows is asynchronous; the
+// device then transposes into the kernels' row-major layout (bf_transpose).
+void narrow_in_order(const Matrix& m, Precision prec, void* dst) {
+  const long n = m.rows() * m.cols();
   const double* src = m.data();
-  parallel_rows(R, 64, [&](long r0, long r1) {
-    constexpr long TB = 32;
-    for (long i0 = r0; i0 < r1; i0 += TB)
-      for (long j0 = 0; j0 < C; j0 += TB) {
-        const long i1 = std::min(r1, i0 + TB), j1 = std::min(C, j0 + TB);
-        for (long i = i0; i < i1; ++i)
-          for (long j = j0; j < j1; ++j) {
-            const float f = static_cast<float>(src[j * R + i]);
-            if (prec == Precision::BF16)
-              static_cast<uint16_t*>(dst)[i * C + j] = to_bf16(f);
-            else
-              static_cast<float*>(dst)[i * C + j] = f;
-          }
-      }
+  parallel_rows(n, 1L << 16, [&](long a, long b) {
+    if (prec == Precision::BF16) {
+      uint16_t* d = static_cast<uint16_t*>(dst);
+      for (long i = a; i < b; ++i) d[i] = to_bf16(static_cast<float>(src[i]));
+    } else {
+      float* d = static_cast<float*>(dst);
+      for (long i = a; i < b; ++i) d[i] = static_cast<float>(src[i]);
+    }
   });
 }
 
-void from_device_layout(const void* src, Matrix& m, Precision prec) {
-  const long R = m.rows(), C = m.cols();
+// The device already transposed the output into column-major order: widen in storage order.
+void widen_in_order(const void* src, Matrix& m, Precision prec) {
+  const long n = m.rows() * m.cols();
   double* dst = m.data();
-  parallel_rows(C, 64, [&](long c0, long c1) {  // column bands: contiguous writes into Eigen storage
-    constexpr long TB = 32;
-    for (long j0 = c0; j0 < c1; j0 += TB)
-      for (long i0 = 0; i0 < R; i0 += TB) {
-        const long j1 = std::min(c1, j0 + TB), i1 = std::min(R, i0 + TB);
-        for (long j = j0; j < j1; ++j)
-          for (long i = i0; i < i1; ++i)
-            dst[j * R + i] = prec == Precision::BF16 ? from_bf16(static_cast<const uint16_t*>(src)[i * C + j])
-                                                     : static_cast<const float*>(src)[i * C + j];
-      }
+  parallel_rows(n, 1L << 16, [&](long a, long b) {
+    if (prec == Precision::BF16) {
+      const uint16_t* s16 = static_cast<const uint16_t*>(src);
+      for (long i = a; i < b; ++i) dst[i] = from_bf16(s16[i]);
+    } else {
+      const float* s32 = static_cast<const float*>(src);
+      for (long i = a; i < b; ++i) dst[i] = s32[i];
+    }
   });
 }
 
@@ -244,14 +238,17 @@ struct Staging {
   std::map<std::pair<int, std::string>, DevBuf> dev;
   int device = 0;
   void* stream = nullptr;
-  // Convert into a pinned buffer, then queue its asynchronous copy: the copy of one input
-  // overlaps the conversion of the next.
+  // Convert into a pinned buffer in Eigen's storage order, queue its asynchronous copy and the
+  // device transpose into row-major: the copy of one input overlaps the conversion of the next.
   void* upload(const std::string& name, const Matrix& m, Precision prec) {
-    const size_t bytes = static_cast<size_t>(m.rows() * m.cols()) * (prec == Precision::BF16 ? 2 : 4);
+    const int eb = prec == Precision::BF16 ? 2 : 4;
+    const size_t bytes = static_cast<size_t>(m.rows() * m.cols()) * eb;
     void* h = host[name].get(bytes);
-    to_device_layout(m, prec, h);
+    narrow_in_order(m, prec, h);
+    void* staged = dev[{device, name + "/colmajor"}].get(bytes);
+    check(bf_copy_to_device(staged, h, bytes, stream), "copy to device");
     void* d = dev[{device, name}].get(bytes);
-    check(bf_copy_to_device(d, h, bytes, stream), "copy to device");
+    check(bf_transpose(staged, d, m.cols(), m.rows(), eb, stream), "transpose to row-major");
     return d;
   }
   void* scratch(const std::string& name, size_t bytes) { return dev[{device, name}].get(bytes); }
@@ -442,7 +439,9 @@ std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const st
   }
   const size_t out_bytes = static_cast<size_t>(out_rows * out_cols) * eb;
   void* host_out = st.host["O"].get(out_bytes);
-  check(bf_copy_to_host(host_out, out, out_bytes, s), "copy to host");
+  void* out_cm = st.scratch("O/colmajor", out_bytes);  // the output in Eigen's storage order
+  check(bf_transpose(out, out_cm, out_rows, out_cols, static_cast<int>(eb), s), "transpose to column-major");
+  check(bf_copy_to_host(host_out, out_cm, out_bytes, s), "copy to host");
   const double t1 = now_ms();
   check(bf_stream_synchronize(s), "stream synchronize");
   const double t2 = now_ms();
@@ -450,7 +449,7 @@ std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const st
   std::map<std::string, Matrix> result;
   Matrix& o = result[rec.output];
   o.resize(out_rows, out_cols);
-  from_device_layout(host_out, o, cfg.precision);
+  widen_in_order(host_out, o, cfg.precision);
   tm.convert_out_ms = now_ms() - t2;
   tm.total_ms = now_ms() - t0;
   tm.h2d_bytes = 0;

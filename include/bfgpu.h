@@ -165,6 +165,12 @@ BF_API int bf_stream_synchronize(void* stream);
 /* Page-locked host memory (cudaHostAlloc, portable): staging for asynchronous copies. */
 BF_API void* bf_host_alloc(size_t bytes);
 BF_API int bf_host_free(void* ptr);
+/* dst = src^T on the device: src is rows x cols row-major, dst cols x rows row-major,
+ * elements of 2, 4 or 8 bytes, stream-ordered. A column-major (Eigen) R x C matrix is a
+ * row-major C x R one, so bindings that hold column-major operands convert element types in
+ * storage order on the host and let this put them in the kernels' row-major layout (and the
+ * output back). Replaces the layout walk of split_into_blocks/assemble (interpreter.hpp:76-138). */
+BF_API int bf_transpose(const void* src, void* dst, int64_t rows, int64_t cols, int elem_bytes, void* stream);
 /* Current device of the calling thread (-1 on error) / select it. */
 BF_API int bf_get_device(void);
 BF_API int bf_set_device(int device);

@@ -75,6 +75,7 @@ _SIGNATURES = [
     ("bf_copy_to_device", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_copy_to_host", ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     ("bf_stream_synchronize", ctypes.c_int, [_vp]),
+    ("bf_transpose", ctypes.c_int, [_vp, _vp, _i64, _i64, ctypes.c_int, _vp]),
     ("bf_host_alloc", ctypes.c_void_p, [ctypes.c_size_t]),
     ("bf_host_free", ctypes.c_int, [_vp]),
     ("bf_get_device", ctypes.c_int, []),
