@@ -438,31 +438,29 @@ def run_reference_arm(args, wl):
     return 0
 
 
-def reference_model(wl: dict, rows: int) -> dict:
-    """The reference's own traffic_bytes model (metrics.hpp:154-191) for this workload."""
+def reference_model(wl: dict, rows: int, workload: str) -> dict:
+    """The reference's own traffic_bytes model (metrics.hpp:154-191) for this workload: the
+    committed values of tests/golden/traffic_model.json (generated from the reference compiled
+    in place, tests/golden/make_traffic_model.py), affine in the number of 128-row M blocks."""
     try:
-        from oracle import refexec as R
-
-        if not R.available():
-            return {"error": "oracle/_ref/libbfref.so not built"}
-        eb = 4 if wl["dtype"] == "f32" else 2
-        if wl["kind"] == "ffn":
-            b = {"M": (rows // 128, 128), "N": (1, wl["N"]), "K": (1, wl["F"]), "D": (1, wl["D"])}
-            which, scale = R.RMS_FFN_SWIGLU, 1
-        elif wl["kind"] == "lnmm":
-            b = {"M": (rows // 128, 128), "K": (1, wl["K"]), "N": (1, wl["N"])}
-            which, scale = R.LAYERNORM_MATMUL, 1
-        else:
-            S, Dh = wl["S"], wl["Dh"]
-            b = {"M": (S // 128, 128), "N": (1, S), "D": (1, Dh), "L": (1, Dh)}
-            which, scale = R.ATTENTION, rows  # per head, times the heads
-        return {"binding": "M in 128-row blocks, contraction dims one block (counts=1)"
-                + (f", per head x {rows} heads" if wl["kind"] == "attn" else ""),
-                "element_bytes": eb,
-                "fused_final_snapshot": scale * R.traffic_bytes(which, R.FINAL, b, eb),
-                "unfused_lowered": scale * R.traffic_bytes(which, R.UNFUSED, b, eb)}
+        tm = json.loads((ROOT / "tests" / "golden" / "traffic_model.json").read_text())["bench_affine_in_m"][workload]
     except Exception as e:  # noqa: BLE001
-        return {"error": str(e)}
+        return {"error": f"tests/golden/traffic_model.json: {e}"}
+    attn = wl["kind"] == "attn"
+    m = wl["S"] // 128 if attn else rows // 128
+    scale = rows if attn else 1
+    snaps = sorted(k for k in tm if k.startswith("snapshot_"))
+
+    def at(name):
+        return scale * (tm[name]["base"] + m * tm[name]["per_m_block"])
+
+    return {"binding": "M in 128-row blocks, contraction dims one block (counts=1)"
+            + (f", per head x {rows} heads" if attn else ""),
+            "element_bytes": tm["element_bytes"],
+            "fused_final_snapshot": at(snaps[-1]),
+            "first_snapshot": at(snaps[0]),
+            "unfused_lowered": at("lowered"),
+            "source": "tests/golden/traffic_model.json"}
 
 
 def e2e_adapter(wl: dict, rows: int, precision: str, schedule: str) -> dict:
@@ -630,7 +628,7 @@ def run_ours(args, wl):
     except Exception as e:  # noqa: BLE001 - reported, not fatal
         plan = {"error": str(e)}
 
-    model = reference_model(wl, inp["rows"]) if rank == 0 else None
+    model = reference_model(wl, inp["rows"], args.workload) if rank == 0 else None
     adapter = None
     if rank == 0 and not args.no_adapter:
         adapter = e2e_adapter(wl, inp["rows"], wl["dtype"], args.schedule)
