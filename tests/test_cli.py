@@ -98,7 +98,7 @@ def test_verify_every_snapshot_against_reference_interpreter(example, dims, bloc
         assert "verdict: equivalent" in r.stdout
 
 
-# the generic float64 GPU route (host/bfgpu_generic.cpp) on programs no fused kernel covers
+# the block-program compiler route, float64 (host/bfgpu_codegen.cpp), on programs no fused kernel covers
 GENERIC = [
     ("attention", "M=2,N=2,D=2,L=2", "4x4", ""),
     ("layernorm-matmul", "M=2,N=2,K=2", "4x4", ""),

@@ -13,9 +13,9 @@
 //                        [--seed 42] [--precision bf16|f32] [--repeat R]
 //   bfgpu-cli verify     <program.json> --dims ... [--block] [--len] [--trials 3]
 //                        [--seed 42] [--tol T] [--precision bf16|f32]
-// run/verify take --route auto|fused|generic: auto runs recognized fused candidates on
-// their sm_100a kernel and anything else (e.g. an unfused lowered.json) on the generic
-// float64 GPU route (host/bfgpu_generic.cpp).
+// run/verify take --route auto|fused|generic: auto runs recognized snapshots on their
+// sm_100a plans and anything else (e.g. an unfused lowered.json) through the block-program
+// compiler, float64 (host/bfgpu_codegen.cpp).
 //
 // `snapshots` is the reference's own fuse(lower(examples::X())) (engine.hpp:164) written
 // with its serializer; it exists because the reference CLI needs CLI11, absent here.
