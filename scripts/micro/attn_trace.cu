@@ -1,7 +1,8 @@
 // Pipeline study for K3: builds attention.cu with BF_ATTN_TRACE and prints per-block
 // SM-clock phase stamps of CTA 0 (softmax WG0/WG1 and the MMA issuer).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DBF_ATTN_TRACE -DBF_ATTN_EMU_FIXED=N
-//        -I include -I paper_2505_07829_b200/csrc scripts/micro/attn_trace.cu -o scripts/micro/attn_trace -lcuda
+//   cd paper_2505_07829_b200/csrc && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DBF_ATTN_TRACE
+//        -I ../../include -I . ../../scripts/micro/attn_trace.cu $(ls *.cu | grep -v '^attention.cu$')
+//        -o ../../scripts/micro/attn_trace -lcuda -ldl -lpthread
 #include <cstdio>
 #include <vector>
 #include <cmath>
@@ -9,12 +10,6 @@
 #include <cstring>
 #include "../../paper_2505_07829_b200/csrc/attention.cu"
 
-namespace bfgpu {
-void note_launch() {}
-void set_last_error(const std::string&) {}
-int current_device() { int d; cudaGetDevice(&d); return d; }
-int num_sms(int d) { int n; cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d); return n; }
-}
 
 int main() {
   const int BH = 256, S = 2048, D = 128;
@@ -40,9 +35,9 @@ int main() {
   cudaMemset(tr, 0, 4 * 64 * 8 * 8);
   bfgpu::attn::attn_trace_buffer = tr;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int it = 0; it < 3; ++it) bfgpu::attention_bf16(Q, K, V, O, BH, S, S, D, D, 0.f, 0);
+  for (int it = 0; it < 3; ++it) bfgpu::attention_bf16(Q, K, V, O, BH, S, S, D, D, 0.f, 0, nullptr, 0, 0);
   cudaEventRecord(e0);
-  for (int it = 0; it < 5; ++it) bfgpu::attention_bf16(Q, K, V, O, BH, S, S, D, D, 0.f, 0);
+  for (int it = 0; it < 5; ++it) bfgpu::attention_bf16(Q, K, V, O, BH, S, S, D, D, 0.f, 0, nullptr, 0, 0);
   cudaEventRecord(e1);
   cudaDeviceSynchronize();
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
