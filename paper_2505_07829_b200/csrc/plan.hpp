@@ -65,6 +65,7 @@ struct Plan {
   int raster = 0;         // K1 down projection: m-units per raster block
   int sync = kSyncNone;
   int emu = 0;            // K3: exponentials per 32 evaluated on the FMA pipe
+  double sched_eff = 0;   // K1: modeled efficiency of the static tile schedule (planner.cu)
   double flops = 0;
   double algo_bytes = 0;  // fused-minimum HBM bytes (inputs + outputs)
   double group_slab_bytes = 0;  // K1: H of one scheduling group; K2: X rows of one group
