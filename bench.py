@@ -653,7 +653,7 @@ def run_ours(args, wl):
         if args.workload == "ffn_70b":
             capture = "prof_ffn70b"  # the C3 capture does not describe the 70B shape
         elif args.workload == "lnmm_c1":
-            capture = "r02_prof_c1"
+            capture = "prof_c1"
         if args.rows:
             capture = None  # captures are taken at the configs' own sizes
         traffic = ncu_traffic(f"{kkey}@{capture}") if capture else None

@@ -92,6 +92,8 @@ struct SplitParams {
 // fits the registers (K <= 1024: 8 float4 per lane), else streamed twice (moments, split).
 __global__ void __launch_bounds__(256) f32_split_kernel(const SplitParams p) {
   constexpr int R = 8;  // float4 per lane held in registers
+  // the GEMM launch may start its prologue now; it waits for this grid before reading
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int warps = static_cast<int>(gridDim.x * blockDim.x / 32);
   const bool vec = (p.K & 3) == 0;
@@ -217,6 +219,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above overlapped the split launch; the split
+  // operands, statistics and colsum are read only after it has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -391,8 +396,18 @@ void lnmm_f32x3(const Plan& pl, const void* X, const void* Yt, void* O, float ep
   gp.O = static_cast<float*>(O);
   ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_gemm_kernel), SMEM_BYTES);
   const dim3 grid(static_cast<unsigned>(2 * ((N + BN - 1) / BN)), static_cast<unsigned>((M + BM - 1) / BM));
-  f32x3_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tm_xh, tm_xl, tm_yh, tm_yl, gp);
-  BF_CUDA(cudaGetLastError());
+  // launched as a programmatic dependent of the split kernel (griddepcontrol in both)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel, tm_xh, tm_xl, tm_yh, tm_yl, gp));
   note_launch();
 }
 
