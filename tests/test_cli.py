@@ -127,6 +127,57 @@ def test_generic_route_runs_unfused_and_every_snapshot(example, dims, block, len
     assert "no CPU fallback" in r.stderr
 
 
+# The driver's peeling route (rule R7, `fuse --enable-peel`, off by default: engine.hpp:22,
+# tools/blockfuse_main.cpp:122-126). Its final rms-swiglu snapshot splits the K map into a
+# First map and a Rest map; with K bound to a single block the Rest range is empty and the
+# reference zero-fills its accumulators from a probe iteration (interpreter.hpp:350-360),
+# the case tests/acceptance.cpp:590-594 checks ("peeling stays sound when the remainder is empty").
+PEEL = PROGRAMS / "rms-swiglu-peel"
+
+
+def test_peel_route_files_regenerate_identically(tmp_path):
+    cli("snapshots", "rms-swiglu", "--out-dir", tmp_path, "--enable-peel", check=0)
+    for f in sorted(PEEL.glob("*.json")):
+        assert (tmp_path / f.name).read_text() == f.read_text(), f.name
+    final = json.loads((PEEL / "snapshot_2.json").read_text())
+
+    def ranges(g):
+        for n in g["nodes"]:
+            if n.get("range"):
+                yield n["dim"], n["range"]
+            if n.get("inner"):
+                yield from ranges(n["inner"])
+
+    assert {("K", "first"), ("K", "rest")} <= set(ranges(final["graph"]))
+    # the first snapshot is the default route's first snapshot (recognized, H buffered); the
+    # peeled final snapshot is no fused kernel's canonical form, so it goes to the compiler
+    assert (PEEL / "snapshot_1.json").read_text() == (PROGRAMS / "rms-swiglu" / "snapshot_1.json").read_text()
+    assert "no CPU fallback" in cli("recognize", PEEL / "snapshot_2.json", check=1).stderr
+
+
+PEEL_BINDINGS = [
+    ("M=2,N=2,K=2,D=2", "4x4", ""),               # acceptance binding (tests/acceptance.cpp:175-201)
+    ("M=3,N=2,K=4,D=1", "4x4", "M=2,N=3,K=2,D=4"),  # asymmetric (tests/test_engine.cpp:221-238)
+    ("M=2,N=2,K=1,D=2", "4x4", "K=3"),             # singleton K: the Rest map is empty
+    ("M=2,N=3,K=1,D=3", "4x4", "M=5,N=3,K=7,D=2"),  # empty Rest, ragged block lengths
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,block,lens", PEEL_BINDINGS)
+def test_peel_route_on_the_compiler(dims, block, lens):
+    for f in ("snapshot_1.json", "snapshot_2.json"):
+        args = ["verify", PEEL / f, "--dims", dims, "--block", block, "--trials", 2, "--route", "generic"]
+        if lens:
+            args += ["--len", lens]
+        r = cli(*args, check=0)
+        assert "route: generic f64" in r.stdout and "verdict: equivalent" in r.stdout, (f, r.stdout)
+    # auto: the unrecognized peeled snapshot runs on the compiler, never on the CPU
+    r = cli("verify", PEEL / "snapshot_2.json", "--dims", dims, "--block", block, "--trials", 1,
+            *(["--len", lens] if lens else []), check=0)
+    assert "route: generic f64" in r.stdout and "verdict: equivalent" in r.stdout
+
+
 @pytest.mark.gpu
 def test_run_reports_output():
     r = cli("run", PROGRAMS / "rms-swiglu" / "snapshot_3.json", "--dims", "M=2,N=2,K=3,D=2", "--block", "128x128",

@@ -66,13 +66,16 @@ struct Args {
     auto it = opt.find(k);
     return it == opt.end() ? def : it->second;
   }
+  bool has(const std::string& k) const { return opt.count(k) != 0; }
 };
 
 Args parse_args(int argc, char** argv, int first) {
   Args a;
   for (int i = first; i < argc; ++i) {
     std::string s = argv[i];
-    if (s.rfind("--", 0) == 0) {
+    if (s == "--enable-peel") {  // the only flag without a value
+      a.opt["enable-peel"] = "1";
+    } else if (s.rfind("--", 0) == 0) {
       if (i + 1 >= argc) throw Error("option " + s + " needs a value");
       a.opt[s.substr(2)] = argv[++i];
     } else {
@@ -147,7 +150,8 @@ BlockGraph load_block(const std::string& path) {
 }
 
 int cmd_snapshots(const Args& a) {
-  if (a.pos.size() != 1) throw Error("usage: snapshots <attention|layernorm-matmul|rms-swiglu> --out-dir D");
+  if (a.pos.size() != 1)
+    throw Error("usage: snapshots <attention|layernorm-matmul|rms-swiglu> --out-dir D [--enable-peel]");
   const std::string name = a.pos[0];
   ArrayProgram p;
   if (name == "attention")
@@ -163,7 +167,11 @@ int cmd_snapshots(const Args& a) {
   fs::create_directories(dir);
   const BlockGraph lowered = lower(p);
   write_file(dir + "/lowered.json", serialize_program(lowered));
-  FuseResult r = fuse(lowered, EngineConfig{});
+  // --enable-peel: the driver's peeling route (rule R7, off by default), as the reference CLI's
+  // `fuse --enable-peel` (tools/blockfuse_main.cpp:122-126, engine.hpp:22)
+  EngineConfig cfg;
+  cfg.enable_peel = a.has("enable-peel");
+  FuseResult r = fuse(lowered, cfg);
   for (size_t i = 0; i < r.snapshots.size(); ++i)
     write_file(dir + "/snapshot_" + std::to_string(i + 1) + ".json", serialize_program(r.snapshots[i].program));
   std::cout << "{\"example\": \"" << name << "\", \"snapshots\": " << r.snapshots.size() << "}\n";
