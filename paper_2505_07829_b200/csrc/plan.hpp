@@ -88,7 +88,7 @@ std::string plan_json(const Plan& p);
 // Kernel descriptors, defined next to each kernel.
 KernelSpec ffn2_spec();
 KernelSpec ffn1_spec();
-KernelSpec lnmm2_spec();
+KernelSpec lnmm2_spec(bool wide);
 KernelSpec lnmm1_spec();
 KernelSpec attn_spec(int D, int Dv, int emu);
 KernelSpec attn_staged_spec(int D, int Dv);

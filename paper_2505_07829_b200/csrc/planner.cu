@@ -284,8 +284,12 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int sched
     return p;
   }
   const bool one_sm = env_int("BFGPU_LNMM_1SM", 0) == 1 && schedule == BF_SCHED_FUSED;
-  p.spec = one_sm ? lnmm1_spec() : lnmm2_spec();
-  why << (one_sm ? "override BFGPU_LNMM_1SM=1: 1-SM kernel; " : "CTA-pair kernel, 256x256 output tiles; ");
+  const bool wide = !one_sm && env_int("BFGPU_LNMM_WIDE", 0) == 1;
+  p.spec = one_sm ? lnmm1_spec() : lnmm2_spec(wide);
+  why << (one_sm ? "override BFGPU_LNMM_1SM=1: 1-SM kernel; "
+                 : (wide ? "CTA-pair kernel, 512x256 output tiles (two M=256 MMAs per K step, single-buffered "
+                           "TMEM); "
+                         : "CTA-pair kernel, 256x256 output tiles; "));
   const int unit = p.spec.tile_m;
   p.units = cdiv(M, unit);
   p.tiles = p.units * cdiv(N, p.spec.tile_n);

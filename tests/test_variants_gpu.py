@@ -1,5 +1,6 @@
 """Parity of the non-default kernel variants that the environment selects (read once per
 process, hence the subprocesses): the 1-SM K1 and K2 kernels (BFGPU_FFN_1SM, BFGPU_LNMM_1SM),
+the 512x256-tile K2 (BFGPU_LNMM_WIDE),
 the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU), non-default K1/K2 scheduling groups
 (BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP) and the K1 wave sync forced on at a size where it is off by default (BFGPU_FFN_WAVESYNC=1).
 Same oracle and tolerances as the default-path tests."""
@@ -56,6 +57,7 @@ print("ok")
         ("ffn", {"BFGPU_FFN_BRASTER": "3"}),
         ("lnmm", {"BFGPU_LNMM_1SM": "1"}),
         ("lnmm", {"BFGPU_LNMM_GROUP": "2"}),
+        ("lnmm", {"BFGPU_LNMM_WIDE": "1"}),
         ("attn", {"BFGPU_ATTN_EMU": "0"}),
         ("attn", {"BFGPU_ATTN_EMU": "12"}),
         ("attn", {"BFGPU_ATTN_EMU": "16"}),
