@@ -354,9 +354,26 @@ std::map<std::string, Matrix> execute(const BlockGraph& program, const std::map<
   return execute_routed(program, inputs, binding, cfg, blockfuse::ExecOptions{});
 }
 
+// The reference's input errors (eval_graph's Input case, interpreter.hpp:386-403), in its order
+// (top-level Input nodes in topological order), raised before any device work on every route,
+// so a bad call fails the same way with or without a GPU.
+void validate_inputs(const BlockGraph& g, const std::map<std::string, Matrix>& in, const DimBinding& b) {
+  for (blockfuse::NodeId id : blockfuse::topological_order(g)) {
+    const blockfuse::Node& n = g.node(id);
+    if (n.kind != blockfuse::NodeKind::Input) continue;
+    auto it = in.find(n.name);
+    if (it == in.end()) throw Error("missing input matrix " + n.name);
+    if (!n.rows_dim.empty() && it->second.rows() != b.total(n.rows_dim))
+      throw Error("input " + n.name + ": row count does not match binding");
+    if (!n.cols_dim.empty() && it->second.cols() != b.total(n.cols_dim))
+      throw Error("input " + n.name + ": column count does not match binding");
+  }
+}
+
 std::map<std::string, Matrix> execute_routed(const BlockGraph& program, const std::map<std::string, Matrix>& inputs,
                                              const DimBinding& binding, const ExecConfig& cfg,
                                              const blockfuse::ExecOptions& opts) {
+  validate_inputs(program, inputs, binding);
   if (cfg.route == Route::Generic) return execute_generic(program, inputs, binding, opts, cfg.stream);
   Recognized rec;
   try {

@@ -108,6 +108,46 @@ __attribute__((visibility("default"))) int bfx_compare(int which, int snap, cons
   }
 }
 
+// The reference's input errors through both executors on the final snapshot of `which`:
+// kind 0 drops the first input, 1 adds a row to it, 2 adds a column, 3 unbinds dimension M.
+// Writes blockfuse::execute's message to ref and bfgpu::execute's to ours; returns how many
+// of the two threw.
+__attribute__((visibility("default"))) int bfx_error_case(int which, int kind, const char* binding, char* ref,
+                                                          char* ours, int len) {
+  BlockGraph unfused = lower(example(which, 0.0));
+  FuseResult fr = fuse(unfused);
+  const BlockGraph& prog = fr.snapshots.back().program;
+  DimBinding b = parse(binding);
+  auto in = random_inputs(input_specs(unfused, b), 7);
+  auto first = in.begin();
+  if (kind == 0) {
+    in.erase(first);
+  } else if (kind == 1 || kind == 2) {
+    Matrix& m = first->second;
+    Matrix g = Matrix::Zero(m.rows() + (kind == 1), m.cols() + (kind == 2));
+    g.block(0, 0, m.rows(), m.cols()) = m;
+    m = g;
+  } else {
+    b.dims.erase("M");
+  }
+  int threw = 0;
+  set_msg(ref, len, "no error");
+  set_msg(ours, len, "no error");
+  try {
+    execute(prog, in, b);
+  } catch (const std::exception& e) {
+    set_msg(ref, len, e.what());
+    ++threw;
+  }
+  try {
+    bfgpu::execute(prog, in, b);
+  } catch (const std::exception& e) {
+    set_msg(ours, len, e.what());
+    ++threw;
+  }
+  return threw;
+}
+
 // Attention snapshot `snap` on the compiled (generic) route with Q scaled by `qscale`, so the
 // logits leave exp's range: max rel. error vs safe_attention_rows (safe_numerics.hpp:147)
 // in *err, and the reference interpreter's own error (it overflows) in *ref_err.

@@ -112,3 +112,22 @@ def test_adapter_eps(lib):
     rc, rel, norm, msg = compare(lib, FFN, -1, "D=2x128,K=2x128,M=2x128,N=1x128", 1, 9, eps=1e-3)
     assert rc == 0, msg
     assert rel <= F32_REL_TOL
+
+
+# The reference's input errors (eval_graph's Input case, interpreter.hpp:386-403, and
+# DimBinding, :49-58): the drop-in raises the same blockfuse::Error messages, before any device
+# work, so this runs on the CPU. kind 0: an input missing; 1: one row too many; 2: one column
+# too many; 3: dimension M unbound.
+@pytest.mark.parametrize("which", [ATTN, LNMM, FFN])
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_input_errors_match_reference(lib, which, kind):
+    lib.bfx_error_case.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                   ctypes.c_int]
+    binding = {ATTN: b"M=2x4,N=2x4,D=2x4,L=2x4", LNMM: b"M=2x4,N=2x4,K=2x4", FFN: b"M=2x4,N=2x4,D=2x4,K=2x4"}[which]
+    ref, ours = ctypes.create_string_buffer(512), ctypes.create_string_buffer(512)
+    threw = lib.bfx_error_case(which, kind, binding, ref, ours, 512)
+    assert threw == 2, (ref.value, ours.value)
+    assert ours.value == ref.value
+    expect = {0: b"missing input matrix", 1: b"row count does not match binding",
+              2: b"column count does not match binding", 3: b"unbound dimension M"}[kind]
+    assert expect in ref.value
