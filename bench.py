@@ -515,8 +515,15 @@ def run_ours(args, wl):
     from paper_2505_07829_b200 import ops
 
     rank, world, local = dist_info()
+    # one GPU per rank; BFGPU_BENCH_BACKEND=gloo with more ranks than GPUs is a functional test of
+    # the multi-rank path on one device (ranks then time-share it), never a measurement
+    backend = os.environ.get("BFGPU_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     peaks, peaks_src = load_peaks()
