@@ -10,6 +10,7 @@
 #include "blockfuse/engine.hpp"
 #include "blockfuse/lowering.hpp"
 #include "blockfuse/safe_numerics.hpp"
+#include "test_util.hpp"  // the reference's own test programs (proj/tests, compiled in place)
 
 using namespace blockfuse;
 
@@ -146,6 +147,116 @@ __attribute__((visibility("default"))) int bfx_error_case(int which, int kind, c
     ++threw;
   }
   return threw;
+}
+
+// The reference interpreter's own test programs (tests/test_interpreter.cpp:46-178, built by
+// tests/test_util.hpp) through the block-program compiler, against blockfuse::execute on the
+// same inputs: 0 identity elementwise, 1 row sums through a map over column blocks and a
+// fold, 2 relu_matmul unfused, 3 relu_matmul fused by hand, 4 the fusion driver's final
+// snapshot of relu_matmul, 5 a top-level Misc node with a host executor, 6 relu_matmul with
+// its M blocks permuted (the output rows must permute the same way: iteration order does not
+// matter). *err = max|ours - ref| / max|ref|.
+__attribute__((visibility("default"))) int bfx_interp_case(int which, double* err, char* msg, int len) {
+  try {
+    BlockGraph g;
+    std::map<std::string, Matrix> in;
+    DimBinding b;
+    ExecOptions opts;
+    std::string out = "R";
+    auto rnd = [](long r, long c, unsigned long long seed) {
+      auto m = random_inputs({{"x", r, c}}, seed);
+      return m.at("x");
+    };
+    switch (which) {
+      case 0:
+        g = bftest::single_elementwise(0, 1);
+        in["a"] = rnd(4, 4, 7);
+        out = "b";
+        break;
+      case 1: {
+        NodeId x = mk_input(g, g.fresh_id(), "X", ValueDesc::list_of(Base::Block, {"K"}), "", "K");
+        BlockGraph mi;
+        NodeId bi = mk_boundary_in(mi, g.fresh_id());
+        NodeId rs = mk_func(mi, g.fresh_id(), FuncKind::RowSum);
+        NodeId bo = mk_boundary_out(mi, g.fresh_id());
+        mi.connect(bi, 0, rs, 0, ValueDesc::block());
+        mi.connect(rs, 0, bo, 0, ValueDesc::vector());
+        NodeId m = mk_map(g, g.fresh_id(), "K", std::move(mi), {PortMode::Iterate});
+        NodeId red = mk_reduce(g, g.fresh_id());
+        NodeId o = mk_output(g, g.fresh_id(), "S");
+        g.connect(x, 0, m, 0, ValueDesc::list_of(Base::Block, {"K"}));
+        g.connect(m, 0, red, 0, ValueDesc::list_of(Base::Vector, {"K"}));
+        g.connect(red, 0, o, 0, ValueDesc::vector());
+        b.dims["K"] = {3, 2};
+        in["X"] = rnd(4, 6, 3);
+        out = "S";
+        break;
+      }
+      case 2:
+      case 3:
+      case 4:
+      case 6:
+        g = which == 3 ? bftest::relu_matmul(true) : bftest::relu_matmul(false);
+        if (which == 4) g = fuse(g).snapshots.back().program;
+        b.dims["M"] = {3, 2};
+        b.dims["N"] = {2, 2};
+        b.free_len = 4;
+        in["A"] = rnd(6, 4, 13);
+        in["Bt"] = rnd(4, 4, 14);
+        break;
+      case 5: {
+        NodeId a = mk_input(g, g.fresh_id(), "a", ValueDesc::block(), "", "");
+        NodeId misc = mk_misc(g, g.fresh_id(), "reverse_rows");
+        NodeId o = mk_output(g, g.fresh_id(), "b");
+        g.connect(a, 0, misc, 0, ValueDesc::block());
+        g.connect(misc, 0, o, 0, ValueDesc::block());
+        opts.misc["reverse_rows"] = [](const std::vector<Value>& v) {
+          const Matrix& m = v[0].block();
+          Matrix r(m.rows(), m.cols());
+          for (long i = 0; i < m.rows(); ++i)
+            for (long j = 0; j < m.cols(); ++j) r(i, j) = m(m.rows() - 1 - i, j);
+          return std::vector<Value>{Value(std::move(r))};
+        };
+        in["a"] = rnd(3, 3, 11);
+        out = "b";
+        break;
+      }
+      default:
+        throw Error("unknown case");
+    }
+    bfgpu::ExecConfig cfg;
+    cfg.precision = bfgpu::Precision::F32;
+    cfg.route = bfgpu::Route::Generic;
+    Matrix got = bfgpu::execute_routed(g, in, b, cfg, opts).at(out);
+    Matrix ref = execute(g, in, b, opts).at(out);
+    if (which == 6) {  // permute A's row blocks (2 rows each): blocks 2, 0, 1
+      std::map<std::string, Matrix> inp = in;
+      Matrix& a = inp["A"];
+      const Matrix a0 = in.at("A");
+      const int order[3] = {2, 0, 1};
+      for (int blk = 0; blk < 3; ++blk)
+        for (long i = 0; i < 2; ++i)
+          for (long j = 0; j < a0.cols(); ++j) a(2 * blk + i, j) = a0(2 * order[blk] + i, j);
+      got = bfgpu::execute_routed(g, inp, b, cfg, opts).at(out);
+      Matrix perm = ref;
+      for (int blk = 0; blk < 3; ++blk)
+        for (long i = 0; i < 2; ++i)
+          for (long j = 0; j < ref.cols(); ++j) perm(2 * blk + i, j) = ref(2 * order[blk] + i, j);
+      ref = perm;
+    }
+    double md = 0, mr = 0;
+    for (long i = 0; i < ref.rows(); ++i)
+      for (long j = 0; j < ref.cols(); ++j) {
+        md = std::max(md, std::abs(got(i, j) - ref(i, j)));
+        mr = std::max(mr, std::abs(ref(i, j)));
+      }
+    *err = md / std::max(mr, 1e-300);
+    set_msg(msg, len, "ok");
+    return 0;
+  } catch (const std::exception& e) {
+    set_msg(msg, len, e.what());
+    return 1;
+  }
 }
 
 // Attention snapshot `snap` on the compiled (generic) route with Q scaled by `qscale`, so the

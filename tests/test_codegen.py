@@ -121,3 +121,22 @@ print(rc, got.value, safe.value, msg.value.decode())
             assert float(err) < 1e-10, r.stdout  # max rel. error vs safe_attention_rows
         else:
             assert err in ("nan", "inf") or float(err) > 1e-3, r.stdout
+
+
+# The reference interpreter's own test programs (tests/test_interpreter.cpp:46-178, via
+# tests/test_util.hpp) through the compiler, against blockfuse::execute on the same inputs.
+INTERP_CASES = {0: "identity elementwise", 1: "row sums: map over column blocks + fold",
+                2: "relu_matmul unfused", 3: "relu_matmul fused by hand", 4: "relu_matmul, driver's final snapshot",
+                5: "top-level Misc node with a host executor", 6: "map iteration order (permuted M blocks)"}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(INTERP_CASES))
+def test_reference_interpreter_programs_on_the_compiler(libs, case):
+    l, _ = libs
+    l.bfx_interp_case.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, ctypes.c_int]
+    err = ctypes.c_double()
+    msg = ctypes.create_string_buffer(1024)
+    rc = l.bfx_interp_case(case, ctypes.byref(err), msg, 1024)
+    assert rc == 0, f"{INTERP_CASES[case]}: {msg.value.decode()}"
+    assert err.value <= 1e-12, f"{INTERP_CASES[case]}: max rel err {err.value:.3e}"
