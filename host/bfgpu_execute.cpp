@@ -7,6 +7,7 @@
 // binding totals, lay it out row-major for the device (Eigen storage is
 // column-major), run the recognized kernel, and return the named output.
 #include "bfgpu_execute.hpp"
+#include "convert.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -122,21 +123,6 @@ std::string output_name(const BlockGraph& g) {
 
 // ------------------------------------------------------------------ layout
 
-uint16_t to_bf16(float f) {
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40u);  // NaN stays NaN
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return static_cast<uint16_t>(u >> 16);
-}
-
-float from_bf16(uint16_t h) {
-  const uint32_t u = static_cast<uint32_t>(h) << 16;
-  float f;
-  std::memcpy(&f, &u, 4);
-  return f;
-}
-
 int host_threads() {
   static const int n = [] {
     const char* v = std::getenv("BFGPU_HOST_THREADS");
@@ -161,18 +147,21 @@ void parallel_rows(long n, long grain, Fn fn) {
 }
 
 // Column-major Eigen storage -> the same storage order in bf16/fp32 (a contiguous pass, split
-// across the host threads). `dst` is page-locked so the copy that follows is asynchronous; the
-// device then transposes into the kernels' row-major layout (bf_transpose).
+// across the host threads, AVX2). `dst` is page-locked so the copy that follows is
+// asynchronous; the device then transposes into the kernels' row-major layout (bf_transpose).
 void narrow_in_order(const Matrix& m, Precision prec, void* dst) {
   const long n = m.rows() * m.cols();
   const double* src = m.data();
   parallel_rows(n, 1L << 16, [&](long a, long b) {
+    long i = a;
     if (prec == Precision::BF16) {
       uint16_t* d = static_cast<uint16_t*>(dst);
-      for (long i = a; i < b; ++i) d[i] = to_bf16(static_cast<float>(src[i]));
+      for (; i + 8 <= b; i += 8) _mm_storeu_si128(reinterpret_cast<__m128i*>(d + i), conv::bf16x8_from_f64(src + i));
+      for (; i < b; ++i) d[i] = conv::to_bf16(static_cast<float>(src[i]));
     } else {
       float* d = static_cast<float*>(dst);
-      for (long i = a; i < b; ++i) d[i] = static_cast<float>(src[i]);
+      for (; i + 4 <= b; i += 4) _mm_storeu_ps(d + i, _mm256_cvtpd_ps(_mm256_loadu_pd(src + i)));
+      for (; i < b; ++i) d[i] = static_cast<float>(src[i]);
     }
   });
 }
@@ -182,12 +171,15 @@ void widen_in_order(const void* src, Matrix& m, Precision prec) {
   const long n = m.rows() * m.cols();
   double* dst = m.data();
   parallel_rows(n, 1L << 16, [&](long a, long b) {
+    long i = a;
     if (prec == Precision::BF16) {
       const uint16_t* s16 = static_cast<const uint16_t*>(src);
-      for (long i = a; i < b; ++i) dst[i] = from_bf16(s16[i]);
+      for (; i + 8 <= b; i += 8) conv::f64x8_from_bf16(s16 + i, dst + i);
+      for (; i < b; ++i) dst[i] = conv::from_bf16(s16[i]);
     } else {
       const float* s32 = static_cast<const float*>(src);
-      for (long i = a; i < b; ++i) dst[i] = s32[i];
+      for (; i + 4 <= b; i += 4) _mm256_storeu_pd(dst + i, _mm256_cvtps_pd(_mm_loadu_ps(s32 + i)));
+      for (; i < b; ++i) dst[i] = s32[i];
     }
   });
 }

@@ -2,11 +2,14 @@
 // blockfuse::execute (the reference CPU executor) on the reference's own
 // programs and random_inputs, exposed as C for tests/test_execute_gpu.py.
 #include <cmath>
+#include <random>
+#include <vector>
 #include <limits>
 #include <cstring>
 #include <string>
 
 #include "bfgpu_execute.hpp"
+#include "convert.hpp"
 #include "blockfuse/engine.hpp"
 #include "blockfuse/lowering.hpp"
 #include "blockfuse/safe_numerics.hpp"
@@ -147,6 +150,49 @@ __attribute__((visibility("default"))) int bfx_error_case(int which, int kind, c
     ++threw;
   }
   return threw;
+}
+
+// The adapter's AVX2 conversions against their scalar forms, bit for bit, on n values mixing
+// normals of every magnitude, rounding ties, subnormals, infinities and NaNs. Returns the number
+// of mismatching elements (narrowing to bf16, and widening back).
+__attribute__((visibility("default"))) long bfx_conversion_check(long n, unsigned long long seed) {
+  std::mt19937_64 rng(seed);
+  std::vector<double> x(static_cast<size_t>(n));
+  for (long i = 0; i < n; ++i) {
+    const uint64_t r = rng();
+    switch (r % 8) {
+      case 0: x[i] = std::ldexp(static_cast<double>(static_cast<int64_t>(rng())) / 9.2e18, static_cast<int>(rng() % 300) - 150); break;
+      case 1: {  // an fp32 value exactly halfway between two bf16 values (ties)
+        uint32_t u = static_cast<uint32_t>(rng()) & 0xffff0000u;
+        u |= 0x8000u;
+        float f;
+        std::memcpy(&f, &u, 4);
+        x[i] = std::isfinite(f) ? f : 1.0;
+        break;
+      }
+      case 2: x[i] = std::ldexp(1.0 + static_cast<double>(rng() % 1000) / 1000.0, -130 - static_cast<int>(rng() % 20)); break;
+      case 3: x[i] = (r & 16) ? std::numeric_limits<double>::infinity() : -std::numeric_limits<double>::infinity(); break;
+      case 4: x[i] = std::numeric_limits<double>::quiet_NaN(); break;
+      case 5: x[i] = std::ldexp(static_cast<double>(rng() % 2000000) - 1e6, static_cast<int>(rng() % 40) - 20); break;
+      case 6: x[i] = (r & 16) ? 3.4e38 * 1.01 : -3.4e38 * 1.01; break;  // rounds to +-inf in fp32
+      default: x[i] = static_cast<double>(static_cast<int64_t>(rng())) / 9.2e18; break;
+    }
+  }
+  long bad = 0;
+  std::vector<uint16_t> v(static_cast<size_t>(n));
+  long i = 0;
+  for (; i + 8 <= n; i += 8) _mm_storeu_si128(reinterpret_cast<__m128i*>(v.data() + i), bfgpu::conv::bf16x8_from_f64(x.data() + i));
+  for (; i < n; ++i) v[i] = bfgpu::conv::to_bf16(static_cast<float>(x[i]));
+  for (long k = 0; k < n; ++k)
+    if (v[k] != bfgpu::conv::to_bf16(static_cast<float>(x[k]))) ++bad;
+  std::vector<double> w(static_cast<size_t>(n));
+  for (i = 0; i + 8 <= n; i += 8) bfgpu::conv::f64x8_from_bf16(v.data() + i, w.data() + i);
+  for (; i < n; ++i) w[i] = bfgpu::conv::from_bf16(v[i]);
+  for (long k = 0; k < n; ++k) {
+    const double e = bfgpu::conv::from_bf16(v[k]);
+    if (std::memcmp(&e, &w[k], 8) != 0) ++bad;
+  }
+  return bad;
 }
 
 // The reference interpreter's own test programs (tests/test_interpreter.cpp:46-178, built by

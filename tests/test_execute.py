@@ -131,3 +131,12 @@ def test_input_errors_match_reference(lib, which, kind):
     expect = {0: b"missing input matrix", 1: b"row count does not match binding",
               2: b"column count does not match binding", 3: b"unbound dimension M"}[kind]
     assert expect in ref.value
+
+
+def test_host_conversions_are_bit_exact(lib):
+    """The adapter's AVX2 fp64 -> bf16 narrowing and bf16 -> fp64 widening (host/convert.hpp) equal
+    their scalar forms bit for bit: ties, subnormals, infinities, overflow to inf, NaN."""
+    lib.bfx_conversion_check.argtypes = [ctypes.c_long, ctypes.c_ulonglong]
+    lib.bfx_conversion_check.restype = ctypes.c_long
+    for n, seed in ((1 << 20, 1), (1003, 2), (7, 3)):
+        assert lib.bfx_conversion_check(n, seed) == 0
