@@ -55,7 +55,7 @@ void ffn_swiglu_bf16(const void* X, const void* Wt, const void* Vt, const void* 
                      int64_t F, int64_t N, float eps, int schedule, void* ws, size_t ws_bytes, cudaStream_t stream);
 void ffn_swiglu_f32(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
                     int64_t F, int64_t N, float eps, void* ws, size_t ws_bytes, cudaStream_t stream);
-size_t ffn_f32_workspace_bytes(int64_t M, int64_t F);
+size_t ffn_f32_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N);
 
 size_t lnmm_workspace_bytes(int64_t M, int64_t K, int64_t N, int dtype);
 void lnmm_bf16(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int64_t N, float eps, int schedule,
@@ -91,7 +91,7 @@ int bf_device_supported(int device) {
 size_t bf_rms_ffn_swiglu_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N, int dtype, int schedule) {
   (void)schedule;
   if (M <= 0 || D <= 0 || F <= 0 || N <= 0) return 0;
-  return dtype == BF_DTYPE_F32 ? ffn_f32_workspace_bytes(M, F) : ffn_workspace_bytes(M, D, F, N);
+  return dtype == BF_DTYPE_F32 ? ffn_f32_workspace_bytes(M, D, F, N) : ffn_workspace_bytes(M, D, F, N);
 }
 
 int bf_rms_ffn_swiglu(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,

@@ -41,15 +41,9 @@ namespace f32x3 {
 // split over a CTA pair (cluster of 2), so a 1024^2 output still fills 128 SMs; the pair sums
 // its two accumulators through distributed shared memory in a fixed order (deterministic).
 constexpr int BM = 128, BN = 128, BK = 32;  // BK fp32 = one 128-byte swizzle row
-constexpr int STAGES = 3;
 constexpr int A_BYTES = BM * BK * 4;  // 16 KB
 constexpr int B_BYTES = BN * BK * 4;  // 16 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int RED_PITCH = BN * 4 + 16;  // reduction buffer row pitch (bytes): rows land on distinct banks
-static_assert(BM * RED_PITCH <= STAGES * STAGE_BYTES, "reduction buffer reuses the operand ring");
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256;
 constexpr int NUM_THREADS = 256;
-constexpr uint32_t TMEM_COLS = BN;
 // kind::tf32 instruction descriptor: D F32, A/B TF32 (format 2), both K-major, N/8, M/16
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
 
@@ -74,58 +68,68 @@ __device__ __forceinline__ float4 ld_cluster_v4(uint32_t addr) {
   return v;
 }
 
+// One operand of the split launch: `rows` rows of `src` ([rows, K] row-major) go to hi/lo
+// ([rows, Kp], tails zero).
+//   kSegLn    LayerNorm rows: moments about the pivot x_0, stat0 = rstd, stat1 = p - mean, and
+//             the row is shifted by the pivot before the split;
+//   kSegRms   RMSNorm rows: stat0 = 1 / sqrt(mean(x^2) + eps), the row split unshifted;
+//   kSegW     weight rows: stat0 (if set) = the row sum (colsum of the transposed operand).
+enum SegKind { kSegLn = 0, kSegRms = 1, kSegW = 2 };
+struct SplitSeg {
+  const float* src;
+  float* hi;
+  float* lo;
+  float* stat0;
+  float* stat1;
+  int rows, K, Kp, kind;
+};
+constexpr int MAX_SEGS = 4;
 struct SplitParams {
-  const float* X;
-  const float* Yt;
-  int M, N, K, Kp;
-  float inv_k, eps;
-  float* xh;
-  float* xl;
-  float* yh;
-  float* yl;
-  float* rstd;
-  float* negdm;   // [M] p - mean (the shift left after subtracting the pivot)
-  float* colsum;  // [N] sum_k Yt[n, k]
+  SplitSeg seg[MAX_SEGS];
+  int nseg, total_rows;
+  float eps;
 };
 
-// One warp per row: rows [0, M) of X, then [M, M + N) of Yt. A row is read once when it
-// fits the registers (K <= 1024: 8 float4 per lane), else streamed twice (moments, split).
-__global__ void __launch_bounds__(256) f32_split_kernel(const SplitParams p) {
+// One warp per row over the concatenated segments. A row is read once when it fits the
+// registers (K <= 1024: 8 float4 per lane), else streamed twice (moments, split).
+__global__ void __launch_bounds__(256) f32_split_kernel(const __grid_constant__ SplitParams p) {
   constexpr int R = 8;  // float4 per lane held in registers
   // the GEMM launch may start its prologue now; it waits for this grid before reading
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int warps = static_cast<int>(gridDim.x * blockDim.x / 32);
-  const bool vec = (p.K & 3) == 0;
-  for (int r = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) / 32); r < p.M + p.N; r += warps) {
-    const bool is_x = r < p.M;
-    const int rr = is_x ? r : r - p.M;
-    const float* src = (is_x ? p.X : p.Yt) + static_cast<size_t>(rr) * p.K;
-    float4* hi = reinterpret_cast<float4*>((is_x ? p.xh : p.yh) + static_cast<size_t>(rr) * p.Kp);
-    float4* lo = reinterpret_cast<float4*>((is_x ? p.xl : p.yl) + static_cast<size_t>(rr) * p.Kp);
+  for (int r = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) / 32); r < p.total_rows; r += warps) {
+    int si = 0, rr = r;
+    while (si + 1 < p.nseg && rr >= p.seg[si].rows) rr -= p.seg[si++].rows;
+    const SplitSeg& sg = p.seg[si];
+    const int K = sg.K;
+    const bool vec = (K & 3) == 0;
+    const float* src = sg.src + static_cast<size_t>(rr) * K;
+    float4* hi = reinterpret_cast<float4*>(sg.hi + static_cast<size_t>(rr) * sg.Kp);
+    float4* lo = reinterpret_cast<float4*>(sg.lo + static_cast<size_t>(rr) * sg.Kp);
     auto load4 = [&](int k4) -> float4 {  // columns [4 k4, 4 k4 + 4), zero past K
       const int k = 4 * k4;
-      if (vec && k + 3 < p.K) return __ldg(reinterpret_cast<const float4*>(src) + k4);
+      if (vec && k + 3 < K) return __ldg(reinterpret_cast<const float4*>(src) + k4);
       float e[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) e[u] = k + u < p.K ? __ldg(src + k + u) : 0.f;
+      for (int u = 0; u < 4; ++u) e[u] = k + u < K ? __ldg(src + k + u) : 0.f;
       return make_float4(e[0], e[1], e[2], e[3]);
     };
-    const int n4 = p.Kp / 4;
+    const int n4 = sg.Kp / 4;
     const bool in_regs = n4 <= 32 * R;
     float4 v[R];
     if (in_regs) {
 #pragma unroll
       for (int i = 0; i < R; ++i) v[i] = lane + 32 * i < n4 ? load4(lane + 32 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    // moments about the row's first element: no E[x^2] - mu^2 cancellation; for Yt, the sum
-    const float piv = is_x ? __ldg(src) : 0.f;
+    // LayerNorm rows: moments about the row's first element (no E[x^2] - mu^2 cancellation)
+    const float piv = sg.kind == kSegLn ? __ldg(src) : 0.f;
     float s1 = 0.f, s2 = 0.f;
     auto acc = [&](float4 a, int k) {
       const float e[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (k + u < p.K) {
+        if (k + u < K) {
           const float d = e[u] - piv;
           s1 += d;
           s2 = fmaf(d, d, s2);
@@ -143,12 +147,15 @@ __global__ void __launch_bounds__(256) f32_split_kernel(const SplitParams p) {
       s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     }
     if (lane == 0) {
-      if (is_x) {
-        const float dm = s1 * p.inv_k;
-        p.rstd[rr] = 1.0f / sqrtf(s2 * p.inv_k - dm * dm + p.eps);
-        p.negdm[rr] = -dm;
-      } else {
-        p.colsum[rr] = s1;
+      const float inv_k = 1.0f / static_cast<float>(K);
+      if (sg.kind == kSegLn) {
+        const float dm = s1 * inv_k;
+        sg.stat0[rr] = 1.0f / sqrtf(s2 * inv_k - dm * dm + p.eps);
+        sg.stat1[rr] = -dm;
+      } else if (sg.kind == kSegRms) {
+        sg.stat0[rr] = 1.0f / sqrtf(s2 * inv_k + p.eps);  // lowering.hpp:409-411
+      } else if (sg.stat0 != nullptr) {
+        sg.stat0[rr] = s1;
       }
     }
     // x - p: exact when the row sits far from zero (|mu| >> sigma), where centring on a rounded
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(256) f32_split_kernel(const SplitParams p) {
       float h[4], l[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float x = 4 * k4 + u < p.K ? e[u] - piv : 0.f;
+        const float x = 4 * k4 + u < K ? e[u] - piv : 0.f;
         h[u] = tf32_hi(x);
         l[u] = x - h[u];
       }
@@ -175,29 +182,58 @@ __global__ void __launch_bounds__(256) f32_split_kernel(const SplitParams p) {
   }
 }
 
+// GEMM epilogues (one kernel template):
+//   kLn     O = (acc + (p - mean) colsum(Yt)) * rstd                      (K2, rule R5)
+//   kGate   h = silu(rstd * acc_W) * (rstd * acc_V), written as its TF32 split h_hi, h_lo
+//           (the A operand of the down contraction)                       (K1, gate/up)
+//   kPlain  O = acc                                                        (K1, down)
+enum Mode { kLn = 0, kGate = 1, kPlain = 2 };
+
+template <int MODE>
+struct GCfg {
+  static constexpr int NB = MODE == kGate ? 2 : 1;  // B operands sharing the A tile
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + NB * 2 * B_BYTES;
+  static constexpr int STAGES = MODE == kGate ? 2 : 3;
+  static constexpr uint32_t TMEM_COLS = NB * BN;
+  static constexpr int RED_PITCH = NB * BN * 4 + 16;  // reduction row pitch (bytes): rows on distinct banks
+  static_assert(BM * RED_PITCH <= STAGES * STAGE_BYTES, "reduction buffer reuses the operand ring");
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 256;
+  static_assert(SMEM <= 232448, "3xTF32 GEMM SMEM budget");
+};
+
 struct GemmParams {
-  int M, N, kt;
+  int M, N, kt;     // N: output columns written (kGate: the padded F of the down contraction)
+  int Mt, Nt, group;  // tile raster: groups of `group` m-tiles, n slow inside a group
+  int ldo;
   const float* rstd;
   const float* negdm;
   const float* colsum;
-  float* O;
+  float* O;   // kGate: h_hi
+  float* O2;  // kGate: h_lo
 };
 
+template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     f32x3_gemm_kernel(const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
                       const __grid_constant__ CUtensorMap tm_yh, const __grid_constant__ CUtensorMap tm_yl,
+                      const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_vl,
                       const GemmParams p) {
   using namespace dev;
+  using C = GCfg<MODE>;
   extern __shared__ __align__(1024) uint8_t smem[];
   if (smem_u32(smem) & 1023u) __trap();
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();  // which half of K this CTA contracts
-  const int n0 = static_cast<int>(blockIdx.x >> 1) * BN, m0 = static_cast<int>(blockIdx.y) * BM;
+  // grouped raster: the A rows of `group` m-tiles stay in L2 while their n-tiles pass
+  const int t = static_cast<int>(blockIdx.x >> 1);
+  const int per_group = p.group * p.Nt, g = t / per_group, in_g = t % per_group;
+  const int gm = min(p.group, p.Mt - g * p.group);
+  const int m0 = (g * p.group + in_g % gm) * BM, n0 = (in_g / gm) * BN;
   const int khalf = (p.kt + 1) / 2;
   const int k_begin = rank == 0 ? 0 : khalf, k_end = rank == 0 ? khalf : p.kt;
   const int nk = k_end - k_begin;
@@ -207,50 +243,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tm_xl);
     tma_prefetch_desc(&tm_yh);
     tma_prefetch_desc(&tm_yl);
-    for (int s = 0; s < STAGES; ++s) {
+    if constexpr (C::NB == 2) {
+      tma_prefetch_desc(&tm_vh);
+      tma_prefetch_desc(&tm_vl);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // Programmatic dependent launch: everything above overlapped the split launch; the split
-  // operands, statistics and colsum are read only after it has completed.
+  // Programmatic dependent launch: everything above overlapped the previous launch; its
+  // outputs (split operands, statistics, colsum, h) are read only after it has completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
       for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES, k = k_begin + i;
-        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        uint8_t* st = smem + s * STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        const int s = i % C::STAGES, k = k_begin + i;
+        mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         tma_load_2d(&tm_xh, &full[s], st, k * BK, m0);
         tma_load_2d(&tm_xl, &full[s], st + A_BYTES, k * BK, m0);
         tma_load_2d(&tm_yh, &full[s], st + 2 * A_BYTES, k * BK, n0);
         tma_load_2d(&tm_yl, &full[s], st + 2 * A_BYTES + B_BYTES, k * BK, n0);
+        if constexpr (C::NB == 2) {
+          tma_load_2d(&tm_vh, &full[s], st + 2 * A_BYTES + 2 * B_BYTES, k * BK, n0);
+          tma_load_2d(&tm_vl, &full[s], st + 2 * A_BYTES + 3 * B_BYTES, k * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      mbar_wait(&full[s], (i / STAGES) & 1);
+      const int s = i % C::STAGES;
+      mbar_wait(&full[s], (i / C::STAGES) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t xh = smem_u32(smem + s * STAGE_BYTES), xl = xh + A_BYTES, yh = xh + 2 * A_BYTES,
-                       yl = yh + B_BYTES;
+        const uint32_t xh = smem_u32(smem + s * C::STAGE_BYTES), xl = xh + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 bytes per MMA
-          const uint32_t o = kk * 32;
-          // small terms first: lo*hi, hi*lo, then hi*hi
-          umma_tf32_ss(tmem, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0);
-          umma_tf32_ss(tmem, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1);
-          umma_tf32_ss(tmem, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1);
+        for (int b = 0; b < C::NB; ++b) {
+          const uint32_t yh = xh + 2 * A_BYTES + 2 * b * B_BYTES, yl = yh + B_BYTES, d = tmem + b * BN;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 bytes per MMA
+            const uint32_t o = kk * 32;
+            // small terms first: lo*hi, hi*lo, then hi*hi
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1);
+          }
         }
         umma_commit(&empty[s]);
       }
@@ -267,11 +314,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = 0; c < C::NB * BN / 32; ++c) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c * 32, v);
       tmem_wait_ld();
-      float4* dst = reinterpret_cast<float4*>(red + trow * RED_PITCH + c * 128);
+      float4* dst = reinterpret_cast<float4*>(red + trow * C::RED_PITCH + c * 128);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         dst[i] = nk > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
@@ -285,14 +332,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
     const int row = m0 + static_cast<int>(trow);
-    const uint32_t peer = mapa_shared(smem_u32(red + trow * RED_PITCH), 1);
-    const float r = row < p.M ? __ldg(p.rstd + row) : 0.f, nd = row < p.M ? __ldg(p.negdm + row) : 0.f;
-    float* orow = p.O + static_cast<size_t>(row) * p.N;
-    const bool vec = (p.N & 3) == 0;
+    const uint32_t peer = mapa_shared(smem_u32(red + trow * C::RED_PITCH), 1);
+    float r = 0.f, nd = 0.f;
+    if constexpr (MODE != kPlain) r = row < p.M ? __ldg(p.rstd + row) : 0.f;
+    if constexpr (MODE == kLn) nd = row < p.M ? __ldg(p.negdm + row) : 0.f;
+    float* orow = p.O + static_cast<size_t>(row) * p.ldo;
+    const bool vec = (p.N & 3) == 0 && (p.ldo & 3) == 0;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c * 32, v);
+      uint32_t w[32];
+      if constexpr (C::NB == 2) tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + BN + c * 32, w);
       tmem_wait_ld();
       if (row >= p.M) continue;
 #pragma unroll
@@ -301,15 +352,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const float4 o1 = ld_cluster_v4(peer + c * 128 + i * 16);
         const float a[4] = {__uint_as_float(v[4 * i]) + o1.x, __uint_as_float(v[4 * i + 1]) + o1.y,
                             __uint_as_float(v[4 * i + 2]) + o1.z, __uint_as_float(v[4 * i + 3]) + o1.w};
-        float o[4];
+        float o[4], lo[4];
+        if constexpr (MODE == kGate) {
+          const float4 o2 = ld_cluster_v4(peer + BN * 4 + c * 128 + i * 16);
+          const float b[4] = {__uint_as_float(w[4 * i]) + o2.x, __uint_as_float(w[4 * i + 1]) + o2.y,
+                              __uint_as_float(w[4 * i + 2]) + o2.z, __uint_as_float(w[4 * i + 3]) + o2.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) o[u] = col + u < p.N ? fmaf(nd, __ldg(p.colsum + col + u), a[u]) * r : 0.f;
+          for (int u = 0; u < 4; ++u) {
+            const float gt = a[u] * r;
+            const float h = col + u < p.N ? gt / (1.0f + expf(-gt)) * (b[u] * r) : 0.f;
+            o[u] = tf32_hi(h);
+            lo[u] = h - o[u];
+          }
+        } else if constexpr (MODE == kLn) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) o[u] = col + u < p.N ? fmaf(nd, __ldg(p.colsum + col + u), a[u]) * r : 0.f;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) o[u] = a[u];
+        }
         if (vec && col + 3 < p.N) {
           *reinterpret_cast<float4*>(orow + col) = make_float4(o[0], o[1], o[2], o[3]);
+          if constexpr (MODE == kGate)
+            *reinterpret_cast<float4*>(p.O2 + static_cast<size_t>(row) * p.ldo + col) =
+                make_float4(lo[0], lo[1], lo[2], lo[3]);
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (col + u < p.N) orow[col + u] = o[u];
+            if (col + u < p.N) {
+              orow[col + u] = o[u];
+              if constexpr (MODE == kGate) p.O2[static_cast<size_t>(row) * p.ldo + col + u] = lo[u];
+            }
         }
       }
     }
@@ -318,34 +391,103 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();  // rank 1's SMEM stays alive until rank 0 has read it
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem);
+    tmem_dealloc<C::TMEM_COLS>(tmem);
   }
 }
 
 int64_t padded_k(int64_t K) { return (K + BK - 1) / BK * BK; }
+
+// Largest power of two of m-tiles whose hi/lo A rows (128 x Kp x 8 bytes each) fit a third of L2.
+int raster_group(int64_t Mt, int64_t Kp, int64_t l2_bytes) {
+  const int64_t fit = std::max<int64_t>(1, l2_bytes / 3 / (static_cast<int64_t>(BM) * Kp * 8));
+  int g = 1;
+  while (2 * g <= fit && 2 * g <= Mt) g *= 2;
+  return g;
+}
+
+template <int MODE>
+void launch_gemm(const CUtensorMap (&tm)[6], const GemmParams& gp, cudaStream_t stream) {
+  using C = GCfg<MODE>;
+  ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_gemm_kernel<MODE>), C::SMEM);
+  const int64_t tiles = static_cast<int64_t>(gp.Mt) * gp.Nt;
+  BF_CHECK_ARG(2 * tiles < (1ll << 31), "fp32 mode: too many output tiles for one launch");
+  // launched as a programmatic dependent of the previous launch (griddepcontrol in both)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * tiles));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel<MODE>, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], gp));
+  note_launch();
+}
+
+void launch_split(const SplitParams& sp, int sms, cudaStream_t stream) {
+  const int split_grid = static_cast<int>(std::min<int64_t>((sp.total_rows + 7) / 8, static_cast<int64_t>(sms) * 16));
+  f32_split_kernel<<<split_grid, 256, 0, stream>>>(sp);
+  BF_CUDA(cudaGetLastError());
+  note_launch();
+}
+
+CUtensorMap tmap(const float* base, int64_t rows, int64_t Kp, int box_rows) {
+  return make_tmap_2d(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, Kp, Kp, BK, box_rows);
+}
+
+// Carves consecutive 1024-byte aligned buffers out of the workspace.
+struct Carve {
+  uint8_t* w;
+  size_t used = 0;
+  float* take(size_t floats) {
+    float* r = reinterpret_cast<float*>(w + used);
+    used += align_up(floats * 4, 1024);
+    return r;
+  }
+};
 
 }  // namespace f32x3
 
 size_t lnmm_f32x3_workspace_bytes(int64_t M, int64_t K, int64_t N) {
   const size_t kp = static_cast<size_t>(f32x3::padded_k(K));
   return 2 * align_up(static_cast<size_t>(M) * kp * 4, 1024) + 2 * align_up(static_cast<size_t>(N) * kp * 4, 1024) +
-         2 * align_up(static_cast<size_t>(M) * 4, 256) + align_up(static_cast<size_t>(N) * 4, 256);
+         2 * align_up(static_cast<size_t>(M) * 4, 1024) + align_up(static_cast<size_t>(N) * 4, 1024);
 }
 
-KernelSpec f32x3_gemm_spec() {
+size_t ffn_f32x3_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
+  const size_t dp = static_cast<size_t>(f32x3::padded_k(D)), fp = static_cast<size_t>(f32x3::padded_k(F));
+  auto a = [](size_t floats) { return align_up(floats * 4, 1024); };
+  return 2 * a(M * dp) + 4 * a(F * dp) + 2 * a(N * fp) + 2 * a(M * fp) + a(M);
+}
+
+KernelSpec f32x3_gemm_spec(int mode) {
   using namespace f32x3;
   KernelSpec k;
-  k.name = "f32x3_gemm_kernel";
-  k.func = reinterpret_cast<const void*>(&f32x3_gemm_kernel);
   k.threads = NUM_THREADS;
-  k.smem_bytes = SMEM_BYTES;
-  k.tmem_cols = TMEM_COLS;
   k.cluster = 2;  // the K range of a tile split over a CTA pair
   k.tile_m = BM;
   k.tile_n = BN;
   k.tile_k = BK;
-  k.stages = STAGES;
   k.grid_sync = false;
+  auto fill = [&](auto cfg, const void* func) {
+    using C = decltype(cfg);
+    k.func = func;
+    k.smem_bytes = C::SMEM;
+    k.tmem_cols = C::TMEM_COLS;
+    k.stages = C::STAGES;
+  };
+  if (mode == kGate) {
+    k.name = "f32x3_gemm_kernel<gate>";
+    fill(GCfg<kGate>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kGate>));
+  } else if (mode == kPlain) {
+    k.name = "f32x3_gemm_kernel<plain>";
+    fill(GCfg<kPlain>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kPlain>));
+  } else {
+    k.name = "f32x3_gemm_kernel";
+    fill(GCfg<kLn>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kLn>));
+  }
   return k;
 }
 
@@ -357,58 +499,92 @@ void lnmm_f32x3(const Plan& pl, const void* X, const void* Yt, void* O, float ep
   BF_CHECK_ARG(ws != nullptr && ws_bytes >= lnmm_f32x3_workspace_bytes(M, K, N),
                "bf_layernorm_matmul: workspace too small");
   BF_CHECK_ARG((reinterpret_cast<uintptr_t>(ws) & 15u) == 0, "bf_layernorm_matmul: workspace must be 16-byte aligned");
-  BF_CHECK_ARG((M + BM - 1) / BM <= 65535, "bf_layernorm_matmul: fp32 mode supports up to 65535 x 128 rows");
-  uint8_t* w = static_cast<uint8_t*>(ws);
+  BF_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31), "bf_layernorm_matmul: fp32 mode sizes must fit int32");
+  Carve cv{static_cast<uint8_t*>(ws)};
+  float *xh = cv.take(M * Kp), *xl = cv.take(M * Kp), *yh = cv.take(N * Kp), *yl = cv.take(N * Kp);
+  float *rstd = cv.take(M), *negdm = cv.take(M), *colsum = cv.take(N);
   SplitParams sp{};
-  sp.X = static_cast<const float*>(X);
-  sp.Yt = static_cast<const float*>(Yt);
-  sp.M = static_cast<int>(M);
-  sp.N = static_cast<int>(N);
-  sp.K = static_cast<int>(K);
-  sp.Kp = static_cast<int>(Kp);
-  sp.inv_k = 1.0f / static_cast<float>(K);
+  sp.seg[0] = {static_cast<const float*>(X), xh, xl, rstd, negdm, static_cast<int>(M), static_cast<int>(K),
+               static_cast<int>(Kp), kSegLn};
+  sp.seg[1] = {static_cast<const float*>(Yt), yh, yl, colsum, nullptr, static_cast<int>(N), static_cast<int>(K),
+               static_cast<int>(Kp), kSegW};
+  sp.nseg = 2;
+  sp.total_rows = static_cast<int>(M + N);
   sp.eps = eps;
-  const size_t xb = align_up(static_cast<size_t>(M) * Kp * 4, 1024), yb = align_up(static_cast<size_t>(N) * Kp * 4, 1024);
-  sp.xh = reinterpret_cast<float*>(w);
-  sp.xl = reinterpret_cast<float*>(w + xb);
-  sp.yh = reinterpret_cast<float*>(w + 2 * xb);
-  sp.yl = reinterpret_cast<float*>(w + 2 * xb + yb);
-  sp.rstd = reinterpret_cast<float*>(w + 2 * xb + 2 * yb);
-  sp.negdm = sp.rstd + align_up(static_cast<size_t>(M) * 4, 256) / 4;
-  sp.colsum = sp.negdm + align_up(static_cast<size_t>(M) * 4, 256) / 4;
-  const int64_t rows = M + N;
-  const int split_grid = static_cast<int>(std::min<int64_t>((rows + 7) / 8, static_cast<int64_t>(pl.dev.sms) * 16));
-  f32_split_kernel<<<split_grid, 256, 0, stream>>>(sp);
-  BF_CUDA(cudaGetLastError());
-  note_launch();
+  launch_split(sp, pl.dev.sms, stream);
 
-  const CUtensorMap tm_xh = make_tmap_2d(sp.xh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, Kp, Kp, BK, BM);
-  const CUtensorMap tm_xl = make_tmap_2d(sp.xl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, Kp, Kp, BK, BM);
-  const CUtensorMap tm_yh = make_tmap_2d(sp.yh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, N, Kp, Kp, BK, BN);
-  const CUtensorMap tm_yl = make_tmap_2d(sp.yl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, N, Kp, Kp, BK, BN);
+  const CUtensorMap tm[6] = {tmap(xh, M, Kp, BM), tmap(xl, M, Kp, BM), tmap(yh, N, Kp, BN),
+                             tmap(yl, N, Kp, BN), tmap(yh, N, Kp, BN), tmap(yl, N, Kp, BN)};
   GemmParams gp{};
   gp.M = static_cast<int>(M);
   gp.N = static_cast<int>(N);
+  gp.ldo = static_cast<int>(N);
   gp.kt = static_cast<int>(Kp / BK);
-  gp.rstd = sp.rstd;
-  gp.negdm = sp.negdm;
-  gp.colsum = sp.colsum;
+  gp.Mt = static_cast<int>((M + BM - 1) / BM);
+  gp.Nt = static_cast<int>((N + BN - 1) / BN);
+  gp.group = raster_group(gp.Mt, Kp, pl.dev.l2_bytes);
+  gp.rstd = rstd;
+  gp.negdm = negdm;
+  gp.colsum = colsum;
   gp.O = static_cast<float*>(O);
-  ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_gemm_kernel), SMEM_BYTES);
-  const dim3 grid(static_cast<unsigned>(2 * ((N + BN - 1) / BN)), static_cast<unsigned>((M + BM - 1) / BM));
-  // launched as a programmatic dependent of the split kernel (griddepcontrol in both)
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel, tm_xh, tm_xl, tm_yh, tm_yl, gp));
-  note_launch();
+  launch_gemm<kLn>(tm, gp, stream);
+}
+
+// K1 fp32 mode on the tensor cores: split {X (RMSNorm rows), Wt, Vt, Ut}, then the gate/up GEMM
+// (two B operands sharing each A tile, SwiGLU epilogue writing h as its TF32 split), then the
+// down GEMM on (h_hi, h_lo) x (u_hi, u_lo). Three launches chained by programmatic dependent launch.
+void ffn_f32x3(const Plan& pl, const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, float eps,
+               void* ws, size_t ws_bytes, cudaStream_t stream) {
+  using namespace f32x3;
+  const int64_t M = pl.dims[0], D = pl.dims[1], F = pl.dims[2], N = pl.dims[3];
+  const int64_t Dp = padded_k(D), Fp = padded_k(F);
+  BF_CHECK_ARG(ws != nullptr && ws_bytes >= ffn_f32x3_workspace_bytes(M, D, F, N),
+               "bf_rms_ffn_swiglu: workspace too small");
+  BF_CHECK_ARG((reinterpret_cast<uintptr_t>(ws) & 15u) == 0, "bf_rms_ffn_swiglu: workspace must be 16-byte aligned");
+  BF_CHECK_ARG(M + 2 * F + N < (1ll << 31), "bf_rms_ffn_swiglu: fp32 mode sizes must fit int32");
+  Carve cv{static_cast<uint8_t*>(ws)};
+  float *xh = cv.take(M * Dp), *xl = cv.take(M * Dp);
+  float *wh = cv.take(F * Dp), *wl = cv.take(F * Dp), *vh = cv.take(F * Dp), *vl = cv.take(F * Dp);
+  float *uh = cv.take(N * Fp), *ul = cv.take(N * Fp), *hh = cv.take(M * Fp), *hl = cv.take(M * Fp);
+  float* rstd = cv.take(M);
+  const int m = static_cast<int>(M), d = static_cast<int>(D), f = static_cast<int>(F), n = static_cast<int>(N);
+  SplitParams sp{};
+  sp.seg[0] = {static_cast<const float*>(X), xh, xl, rstd, nullptr, m, d, static_cast<int>(Dp), kSegRms};
+  sp.seg[1] = {static_cast<const float*>(Wt), wh, wl, nullptr, nullptr, f, d, static_cast<int>(Dp), kSegW};
+  sp.seg[2] = {static_cast<const float*>(Vt), vh, vl, nullptr, nullptr, f, d, static_cast<int>(Dp), kSegW};
+  sp.seg[3] = {static_cast<const float*>(Ut), uh, ul, nullptr, nullptr, n, f, static_cast<int>(Fp), kSegW};
+  sp.nseg = 4;
+  sp.total_rows = static_cast<int>(M + 2 * F + N);
+  sp.eps = eps;
+  launch_split(sp, pl.dev.sms, stream);
+
+  const CUtensorMap tg[6] = {tmap(xh, M, Dp, BM), tmap(xl, M, Dp, BM), tmap(wh, F, Dp, BN),
+                             tmap(wl, F, Dp, BN), tmap(vh, F, Dp, BN), tmap(vl, F, Dp, BN)};
+  GemmParams g1{};
+  g1.M = m;
+  g1.N = static_cast<int>(Fp);  // columns [F, Fp) of h are written as zeros (the down GEMM's K padding)
+  g1.ldo = static_cast<int>(Fp);
+  g1.kt = static_cast<int>(Dp / BK);
+  g1.Mt = static_cast<int>((M + BM - 1) / BM);
+  g1.Nt = static_cast<int>((Fp + BN - 1) / BN);
+  g1.group = raster_group(g1.Mt, Dp, pl.dev.l2_bytes);
+  g1.rstd = rstd;
+  g1.O = hh;
+  g1.O2 = hl;
+  launch_gemm<kGate>(tg, g1, stream);
+
+  const CUtensorMap td[6] = {tmap(hh, M, Fp, BM), tmap(hl, M, Fp, BM), tmap(uh, N, Fp, BN),
+                             tmap(ul, N, Fp, BN), tmap(uh, N, Fp, BN), tmap(ul, N, Fp, BN)};
+  GemmParams g2{};
+  g2.M = m;
+  g2.N = n;
+  g2.ldo = n;
+  g2.kt = static_cast<int>(Fp / BK);
+  g2.Mt = g1.Mt;
+  g2.Nt = static_cast<int>((N + BN - 1) / BN);
+  g2.group = raster_group(g2.Mt, Fp, pl.dev.l2_bytes);
+  g2.O = static_cast<float*>(O);
+  launch_gemm<kPlain>(td, g2, stream);
 }
 
 }  // namespace bfgpu

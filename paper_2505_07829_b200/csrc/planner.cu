@@ -186,14 +186,24 @@ static Plan make_plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype,
   p.algo_bytes = eb * (static_cast<double>(M) * D + 2.0 * F * D + static_cast<double>(N) * F + static_cast<double>(M) * N);
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
-    p.spec = simt_gemm_spec(1);
+    const bool simt = env_int("BFGPU_F32_SIMT", 0) == 1;
+    p.spec = simt ? simt_gemm_spec(1) : f32x3_gemm_spec(1);
     p.units = cdiv(M, p.spec.tile_m);
     p.tiles = p.units * (cdiv(F, p.spec.tile_n) + cdiv(N, p.spec.tile_n));
     p.resident_ctas = resident_ctas(p.spec);
-    p.grid = static_cast<int>(std::min<int64_t>(p.units * cdiv(F, p.spec.tile_n), 1 << 30));
-    p.group_slab_bytes = 4.0 * M * F;
-    why << "fp32 mode: FP32 SIMT FMA (TF32 cannot meet the 1e-4 bar); gate/up+SwiGLU kernel then the down "
-           "contraction, H materialized in the fp32 workspace (" << p.group_slab_bytes / 1e6 << " MB)";
+    p.grid = static_cast<int>(std::min<int64_t>(p.units * cdiv(F, p.spec.tile_n) * p.spec.cluster, 1 << 30));
+    if (simt) {
+      p.group_slab_bytes = 4.0 * M * F;
+      why << "override BFGPU_F32_SIMT=1: FP32 SIMT FMA; gate/up+SwiGLU kernel then the down contraction, H "
+             "materialized in the fp32 workspace (" << p.group_slab_bytes / 1e6 << " MB)";
+    } else {
+      p.group_slab_bytes = 8.0 * M * ((F + 31) / 32 * 32);
+      why << "fp32 mode: 3xTF32 on tcgen05 (x = hi + lo, three TF32 products per K step in the fp32 TMEM "
+             "accumulator); a split launch writes hi/lo of X (with the RMSNorm scale), Wt, Vt, Ut, then the "
+             "gate/up GEMM (two B operands per A tile, SwiGLU epilogue writing h as hi/lo, "
+          << p.group_slab_bytes / 1e6 << " MB) and the down GEMM, 128x128 tiles with the K range split over a CTA "
+             "pair, chained by programmatic dependent launch";
+    }
     p.notes = why.str();
     check_budgets(p);
     return p;
@@ -334,12 +344,16 @@ static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, 
                             static_cast<double>(Skv) * Dv + static_cast<double>(Sq) * Dv);
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
-    p.spec = simt_attn_spec();
+    const bool tiled = attn_f32_tiled_supported(D, Dv);
+    p.spec = tiled ? attn_f32_tiled_spec(static_cast<int>(D), static_cast<int>(Dv)) : simt_attn_spec();
     p.units = cdiv(Sq, p.spec.tile_m);
     p.tiles = p.units * BH;
     p.resident_ctas = resident_ctas(p.spec);
     p.grid = static_cast<int>(std::min<int64_t>(p.tiles, 1 << 30));
-    why << "fp32 mode: FP32 SIMT online softmax, one CTA per (head, 16 query rows)";
+    if (tiled)
+      why << "fp32 mode: FP32 FMA flash attention, one CTA per (head, 64 query rows), key blocks of 64 in SMEM";
+    else
+      why << "fp32 mode: FP32 SIMT online softmax (head dims outside 64/128), one CTA per (head, 16 query rows)";
     p.notes = why.str();
     check_budgets(p);
     return p;

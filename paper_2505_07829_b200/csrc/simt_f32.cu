@@ -446,12 +446,25 @@ KernelSpec simt_attn_spec() {
   return k;
 }
 
-size_t ffn_f32_workspace_bytes(int64_t M, int64_t F) { return align_up(static_cast<size_t>(M) * F * 4, 256); }
+size_t ffn_f32x3_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N);
+void ffn_f32x3(const Plan& pl, const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, float eps,
+               void* ws, size_t ws_bytes, cudaStream_t stream);
+
+// Sized for the 3xTF32 plan (hi/lo operands and h); covers the SIMT override's fp32 H as well.
+size_t ffn_f32_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
+  return ffn_f32x3_workspace_bytes(M, D, F, N);
+}
 
 void ffn_swiglu_f32(const void* X, const void* Wt, const void* Vt, const void* Ut, void* O, int64_t M, int64_t D,
                     int64_t F, int64_t N, float eps, void* ws, size_t ws_bytes, cudaStream_t stream) {
   BF_CHECK_ARG(M > 0 && D > 0 && F > 0 && N > 0, "bf_rms_ffn_swiglu: sizes must be positive");
-  BF_CHECK_ARG(ws != nullptr && ws_bytes >= ffn_f32_workspace_bytes(M, F), "bf_rms_ffn_swiglu: workspace too small");
+  const Plan& pl = plan_ffn(M, D, F, N, BF_DTYPE_F32, BF_SCHED_FUSED);
+  if (pl.spec.tensor) {
+    ffn_f32x3(pl, X, Wt, Vt, Ut, O, eps, ws, ws_bytes, stream);
+    return;
+  }
+  BF_CHECK_ARG(ws != nullptr && ws_bytes >= align_up(static_cast<size_t>(M) * F * 4, 256),
+               "bf_rms_ffn_swiglu: workspace too small");
   float* H = static_cast<float*>(ws);
   simt::launch_gemm<simt::kSwiGLU>(static_cast<const float*>(X), static_cast<const float*>(Wt),
                                    static_cast<const float*>(Vt), H, M, F, D, {1.0f / static_cast<float>(D), eps},
@@ -475,12 +488,20 @@ void lnmm_f32(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int6
                                  static_cast<float*>(O), M, N, K, {1.0f / static_cast<float>(K), eps}, stream);
 }
 
+void attention_f32_tiled(const float* Q, const float* K, const float* Vt, float* O, int64_t BH, int64_t Sq,
+                         int64_t Skv, int64_t D, int64_t Dv, float scale, cudaStream_t stream);
+
 void attention_f32(const void* Q, const void* K, const void* Vt, void* O, int64_t BH, int64_t Sq, int64_t Skv,
                    int64_t D, int64_t Dv, float scale, cudaStream_t stream) {
   BF_CHECK_ARG(BH > 0 && Sq > 0 && Skv > 0 && D > 0 && Dv > 0, "bf_attention: sizes must be positive");
   BF_CHECK_ARG(D <= simt::AMAXD && Dv <= simt::AMAXD, "bf_attention: fp32 mode supports D, Dv <= 256");
   BF_CHECK_ARG(BH <= 65535, "bf_attention: too many heads for one launch");
   if (scale <= 0.f) scale = 1.0f / sqrtf(static_cast<float>(D));
+  if (attn_f32_tiled_supported(D, Dv)) {
+    attention_f32_tiled(static_cast<const float*>(Q), static_cast<const float*>(K), static_cast<const float*>(Vt),
+                        static_cast<float*>(O), BH, Sq, Skv, D, Dv, scale, stream);
+    return;
+  }
   dim3 grid(static_cast<unsigned>((Sq + simt::AQ - 1) / simt::AQ), static_cast<unsigned>(BH));
   simt::attn_f32_kernel<<<grid, simt::ATHREADS, 0, stream>>>(
       static_cast<const float*>(Q), static_cast<const float*>(K), static_cast<const float*>(Vt),

@@ -185,3 +185,49 @@ def test_c1_every_row_fp32(torch_ops):
     out = ops.layernorm_matmul(torch.from_numpy(X).cuda().float(), torch.from_numpy(Yt).cuda().float())
     torch.cuda.synchronize()
     assert_f32_close(out.double().cpu().numpy(), cpu.layernorm_matmul(X, Yt), "C1 fp32 all rows")
+
+
+def test_c3_fp32_tensor_cores(torch_ops):
+    """K1 fp32 mode at the C3 shape (3xTF32 on tcgen05: split launch, gate/up GEMM with the SwiGLU
+    epilogue writing h as hi/lo, down GEMM): one row per 128-row m-tile plus the last row vs the
+    float64 oracle at the 1e-4 bar (contractions of 4096 and 14336)."""
+    torch, ops = torch_ops
+    from oracle import cpu
+
+    M, D, F, N = 8192, 4096, 14336, 4096
+    plan = ops.plan("rms_ffn_swiglu", (M, D, F, N), dtype=torch.float32)
+    assert plan["kernel"].startswith("f32x3_gemm_kernel"), plan
+    g = torch.Generator(device="cuda").manual_seed(41)
+    X = torch.randn(M, D, device="cuda", generator=g)
+    Wt = torch.randn(F, D, device="cuda", generator=g) * D ** -0.5
+    Vt = torch.randn(F, D, device="cuda", generator=g) * D ** -0.5
+    Ut = torch.randn(N, F, device="cuda", generator=g) * F ** -0.5
+    O = ops.rms_ffn_swiglu(X, Wt, Vt, Ut)
+    torch.cuda.synchronize()
+    rows = np.append(stratified_rows(M, 128, 41), M - 1)
+    ref = cpu.rms_ffn_swiglu(X[rows].double().cpu().numpy(), Wt.double().cpu().numpy(), Vt.double().cpu().numpy(),
+                             Ut.double().cpu().numpy())
+    assert_f32_close(O[rows].double().cpu().numpy(), ref, "K1 fp32 C3, one row per m-tile, vs oracle")
+
+
+def test_c2_fp32_every_head(torch_ops):
+    """K3 fp32 mode at the C2 shape (tiled FMA flash attention): every head on two query rows per
+    64-row tile vs float64 on the device, at the 1e-4 bar."""
+    torch, ops = torch_ops
+    g = torch.Generator(device="cuda").manual_seed(42)
+    BH, S, D = 256, 2048, 128
+    Q = torch.randn(BH, S, D, device="cuda", generator=g)
+    K = torch.randn(BH, S, D, device="cuda", generator=g)
+    Vt = torch.randn(BH, D, S, device="cuda", generator=g)
+    O = ops.attention(Q, K, Vt)
+    torch.cuda.synchronize()
+    rows = torch.from_numpy(np.concatenate([stratified_rows(S, 64, 42), stratified_rows(S, 64, 43)])).cuda()
+    md = mr = 0.0
+    for h0 in range(0, BH, 32):
+        q = Q[h0:h0 + 32, rows].double()
+        ref = torch.softmax(q @ K[h0:h0 + 32].double().transpose(1, 2) / D ** 0.5, -1) @ \
+            Vt[h0:h0 + 32].double().transpose(1, 2)
+        md = max(md, float((O[h0:h0 + 32, rows].double() - ref).abs().max()))
+        mr = max(mr, float(ref.abs().max()))
+    from helpers import F32_REL_TOL
+    assert md / mr <= F32_REL_TOL, f"K3 fp32 C2: max|d|/max|ref| = {md / mr:.3e}"
