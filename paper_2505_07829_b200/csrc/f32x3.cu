@@ -20,7 +20,8 @@
 //                      Tails padded to Kp = 32k.
 //   f32x3_gemm_kernel  128 x 128 output tiles, K split over a CTA pair; TMA-fed 3-stage
 //                      ring of {X_hi, X_lo, Y_hi, Y_lo} 32-column slabs (SW128), 3 MMAs per
-//                      K=8 step; rank 1 hands its partial sums over DSMEM and rank 0 writes
+//                      K=8 step; each rank pushes its partial sums of the other rank's column
+//                      half into the peer's SMEM (remote stores), then finalizes its own half:
 //                      O = (acc0 + acc1 - dm colsum(Yt)) * rstd straight to global.
 // Reference: ref::layernorm_matmul (interpreter.hpp:549-551); the block program is the
 // final snapshot of fuse(lower(examples::layernorm_matmul())) (lowering.hpp:573-581).
@@ -62,10 +63,9 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ float4 ld_cluster_v4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 
 // One operand of the split launch: `rows` rows of `src` ([rows, K] row-major) go to hi/lo
@@ -195,7 +195,7 @@ struct GCfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + NB * 2 * B_BYTES;
   static constexpr int STAGES = MODE == kGate ? 2 : 3;
   static constexpr uint32_t TMEM_COLS = NB * BN;
-  static constexpr int RED_PITCH = NB * BN * 4 + 16;  // reduction row pitch (bytes): rows on distinct banks
+  static constexpr int RED_PITCH = NB * (BN / 2) * 4 + 16;  // pushed-half row pitch (bytes): rows on distinct banks
   static_assert(BM * RED_PITCH <= STAGES * STAGE_BYTES, "reduction buffer reuses the operand ring");
   static constexpr int SMEM = STAGES * STAGE_BYTES + 256;
   static_assert(SMEM <= 232448, "3xTF32 GEMM SMEM budget");
@@ -292,6 +292,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const uint32_t yh = xh + 2 * A_BYTES + 2 * b * B_BYTES, yl = yh + B_BYTES, d = tmem + b * BN;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 bytes per MMA
+#ifdef BF_F32X3_DBG_NOMMA  // timing only: the load pipeline alone
+            if (i > 0) continue;
+#endif
             const uint32_t o = kk * 32;
             // small terms first: lo*hi, hi*lo, then hi*hi
             umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0);
@@ -306,61 +309,83 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) umma_commit(tfull);  // nk == 0 (K <= 32 on rank 1): arrives at once, acc unused
     __syncwarp();
   }
+  // Epilogue, split by columns over the pair: rank r finalizes columns [64 r, 64 r + 64) of the
+  // tile. Each rank pushes its partial sums of the other half into the peer's SMEM (remote
+  // stores: no round-trip latency exposed), then adds the peer's pushed half to its own TMEM
+  // half in a fixed order (deterministic). The rings are free once both pairs' MMAs are done.
+  constexpr int HALF = BN / 2;
   const uint32_t q = warp & 3;
   const uint32_t trow = q * 32 + lane;
-  uint8_t* red = smem;  // the operand ring is idle once tfull has fired
-  if (warp >= 4 && rank == 1) {
-    // rank 1 parks its partial sums in its own SMEM for rank 0 (zeros if it had no K steps)
+  const uint32_t tl = tmem + ((q * 32) << 16);
+  uint8_t* red = smem + trow * C::RED_PITCH;  // [C::NB][HALF] floats per row
+  if (warp >= 4) {
     mbar_wait(tfull, 0);
     tc_fence_after();
+  }
+  tc_fence_before();
+  cluster_sync();  // A: both CTAs' accumulators are final and their operand rings idle
+  if (warp >= 4) {
+    const uint32_t dst = mapa_shared(smem_u32(red), rank ^ 1);
 #pragma unroll 1
-    for (int c = 0; c < C::NB * BN / 32; ++c) {
+    for (int c = 0; c < C::NB * 2; ++c) {  // (operand b, 32-column chunk) of the peer's half
+      const int b = c >> 1, col = b * BN + static_cast<int>(rank ^ 1) * HALF + (c & 1) * 32;
       uint32_t v[32];
-      tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c * 32, v);
+      tmem_ld_32x32b_x32(tl + col, v);
       tmem_wait_ld();
-      float4* dst = reinterpret_cast<float4*>(red + trow * C::RED_PITCH + c * 128);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        dst[i] = nk > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                      __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < 8; ++i) {
+        const float4 f = nk > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        st_cluster_v4(dst + (b * HALF + (c & 1) * 32 + 4 * i) * 4, f);
+      }
     }
   }
   tc_fence_before();
-  cluster_sync();  // rank 1's partials are visible cluster-wide
-  if (warp >= 4 && rank == 0) {
-    mbar_wait(tfull, 0);
+  cluster_sync();  // B: the pushed halves are visible; no remote access after this point
+  if (warp >= 4) {
     tc_fence_after();
     const int row = m0 + static_cast<int>(trow);
-    const uint32_t peer = mapa_shared(smem_u32(red + trow * C::RED_PITCH), 1);
     float r = 0.f, nd = 0.f;
     if constexpr (MODE != kPlain) r = row < p.M ? __ldg(p.rstd + row) : 0.f;
     if constexpr (MODE == kLn) nd = row < p.M ? __ldg(p.negdm + row) : 0.f;
     float* orow = p.O + static_cast<size_t>(row) * p.ldo;
     const bool vec = (p.N & 3) == 0 && (p.ldo & 3) == 0;
+    const float4* pushed = reinterpret_cast<const float4*>(red);
+#ifdef BF_F32X3_DBG_NOEPI  // timing only: no reduction or stores
+    if (p.M > 0) goto epi_done;
+#endif
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
+      const int cbase = static_cast<int>(rank) * HALF + c * 32;  // tile column of this chunk
       uint32_t v[32];
-      tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c * 32, v);
+      tmem_ld_32x32b_x32(tl + cbase, v);
       uint32_t w[32];
-      if constexpr (C::NB == 2) tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + BN + c * 32, w);
+      if constexpr (C::NB == 2) tmem_ld_32x32b_x32(tl + BN + cbase, w);
       tmem_wait_ld();
       if (row >= p.M) continue;
+      const bool own = nk > 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int col = n0 + c * 32 + 4 * i;
-        const float4 o1 = ld_cluster_v4(peer + c * 128 + i * 16);
-        const float a[4] = {__uint_as_float(v[4 * i]) + o1.x, __uint_as_float(v[4 * i + 1]) + o1.y,
-                            __uint_as_float(v[4 * i + 2]) + o1.z, __uint_as_float(v[4 * i + 3]) + o1.w};
+        const int col = n0 + cbase + 4 * i;
+        const float4 o1 = pushed[(c * 32 + 4 * i) / 4];
+        float a[4] = {o1.x, o1.y, o1.z, o1.w};
+        if (own) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[u] = __uint_as_float(v[4 * i + u]) + a[u];
+        }
         float o[4], lo[4];
         if constexpr (MODE == kGate) {
-          const float4 o2 = ld_cluster_v4(peer + BN * 4 + c * 128 + i * 16);
-          const float b[4] = {__uint_as_float(w[4 * i]) + o2.x, __uint_as_float(w[4 * i + 1]) + o2.y,
-                              __uint_as_float(w[4 * i + 2]) + o2.z, __uint_as_float(w[4 * i + 3]) + o2.w};
+          const float4 o2 = pushed[(HALF + c * 32 + 4 * i) / 4];
+          float bb[4] = {o2.x, o2.y, o2.z, o2.w};
+          if (own) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bb[u] = __uint_as_float(w[4 * i + u]) + bb[u];
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const float gt = a[u] * r;
-            const float h = col + u < p.N ? gt / (1.0f + expf(-gt)) * (b[u] * r) : 0.f;
+            const float h = col + u < p.N ? gt / (1.0f + expf(-gt)) * (bb[u] * r) : 0.f;
             o[u] = tf32_hi(h);
             lo[u] = h - o[u];
           }
@@ -371,6 +396,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) o[u] = a[u];
         }
+#ifdef BF_F32X3_DBG_NOSTORE  // timing only: reduction without the global stores
+        if (p.M > 0) {
+          if (o[0] == 1234.5f) orow[col] = o[1];
+          continue;
+        }
+#endif
         if (vec && col + 3 < p.N) {
           *reinterpret_cast<float4*>(orow + col) = make_float4(o[0], o[1], o[2], o[3]);
           if constexpr (MODE == kGate)
@@ -386,9 +417,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+#ifdef BF_F32X3_DBG_NOEPI
+  epi_done:;
+#endif
   }
   tc_fence_before();
-  cluster_sync();  // rank 1's SMEM stays alive until rank 0 has read it
+  __syncthreads();  // TMEM reads done before the free
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem);
