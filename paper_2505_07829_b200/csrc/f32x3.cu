@@ -349,7 +349,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     float r = 0.f, nd = 0.f;
     if constexpr (MODE != kPlain) r = row < p.M ? __ldg(p.rstd + row) : 0.f;
     if constexpr (MODE == kLn) nd = row < p.M ? __ldg(p.negdm + row) : 0.f;
-    float* orow = p.O + static_cast<size_t>(row) * p.ldo;
     const bool vec = (p.N & 3) == 0 && (p.ldo & 3) == 0;
     const float4* pushed = reinterpret_cast<const float4*>(red);
 #ifdef BF_F32X3_DBG_NOEPI  // timing only: no reduction or stores
@@ -396,25 +395,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) o[u] = a[u];
         }
-#ifdef BF_F32X3_DBG_NOSTORE  // timing only: reduction without the global stores
-        if (p.M > 0) {
-          if (o[0] == 1234.5f) orow[col] = o[1];
-          continue;
-        }
-#endif
-        if (vec && col + 3 < p.N) {
-          *reinterpret_cast<float4*>(orow + col) = make_float4(o[0], o[1], o[2], o[3]);
-          if constexpr (MODE == kGate)
-            *reinterpret_cast<float4*>(p.O2 + static_cast<size_t>(row) * p.ldo + col) =
-                make_float4(lo[0], lo[1], lo[2], lo[3]);
-        } else {
+        // stage in place (this thread's own row of the pushed buffer) for coalesced stores
+        float4* st = reinterpret_cast<float4*>(red) + (c * 32 + 4 * i) / 4;
+        st[0] = make_float4(o[0], o[1], o[2], o[3]);
+        if constexpr (MODE == kGate) st[HALF / 4] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      }
+    }
+    __syncwarp();
+    // the warp's 32 rows x 64 columns, two rows per instruction (256 contiguous bytes each)
+    const int cc = (lane & 15) * 4, col = n0 + static_cast<int>(rank) * HALF + cc;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      const int rl = 2 * k + static_cast<int>(lane >> 4), row2 = m0 + static_cast<int>(q) * 32 + rl;
+      if (row2 >= p.M) break;
+      const uint8_t* srow = smem + (q * 32 + rl) * C::RED_PITCH;
+      const float4 val = *reinterpret_cast<const float4*>(srow + cc * 4);
+      float* out = p.O + static_cast<size_t>(row2) * p.ldo + col;
+      float4 lv;
+      if constexpr (MODE == kGate) lv = *reinterpret_cast<const float4*>(srow + (HALF + cc) * 4);
+      if (vec && col + 3 < p.N) {
+        *reinterpret_cast<float4*>(out) = val;
+        if constexpr (MODE == kGate) *reinterpret_cast<float4*>(p.O2 + static_cast<size_t>(row2) * p.ldo + col) = lv;
+      } else {
+        const float e[4] = {val.x, val.y, val.z, val.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (col + u < p.N) {
-              orow[col + u] = o[u];
-              if constexpr (MODE == kGate) p.O2[static_cast<size_t>(row) * p.ldo + col + u] = lo[u];
+        for (int u = 0; u < 4; ++u)
+          if (col + u < p.N) {
+            out[u] = e[u];
+            if constexpr (MODE == kGate) {
+              const float l4[4] = {lv.x, lv.y, lv.z, lv.w};
+              p.O2[static_cast<size_t>(row2) * p.ldo + col + u] = l4[u];
             }
-        }
+          }
       }
     }
 #ifdef BF_F32X3_DBG_NOEPI
