@@ -403,9 +403,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     __syncwarp();
     // the warp's 32 rows x 64 columns, two rows per instruction (256 contiguous bytes each)
-    const int cc = (lane & 15) * 4, col = n0 + static_cast<int>(rank) * HALF + cc;
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
+      const int cc = (lane & 15) * 4, col = n0 + static_cast<int>(rank) * HALF + cc;
       const int rl = 2 * k + static_cast<int>(lane >> 4), row2 = m0 + static_cast<int>(q) * 32 + rl;
       if (row2 >= p.M) break;
       const uint8_t* srow = smem + (q * 32 + rl) * C::RED_PITCH;

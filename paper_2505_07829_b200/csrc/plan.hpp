@@ -97,6 +97,9 @@ KernelSpec f32x3_gemm_spec(int mode = 0);  // 0 LayerNorm epilogue, 1 gate/up + 
 KernelSpec simt_attn_spec();
 KernelSpec attn_f32_tiled_spec(int D, int Dv);
 bool attn_f32_tiled_supported(int64_t D, int64_t Dv);
+KernelSpec attn_f32x3_spec(int D, int Dv);
+bool attn_f32x3_supported(int64_t D, int64_t Dv, int64_t Skv, const void* Q, const void* K, const void* Vt,
+                          const void* O);  // Q == nullptr: shape check only
 
 extern void note_launch();
 

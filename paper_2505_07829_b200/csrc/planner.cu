@@ -344,13 +344,19 @@ static Plan make_plan_attention(int64_t BH, int64_t Sq, int64_t Skv, int64_t D, 
                             static_cast<double>(Skv) * Dv + static_cast<double>(Sq) * Dv);
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
-    const bool tiled = attn_f32_tiled_supported(D, Dv);
-    p.spec = tiled ? attn_f32_tiled_spec(static_cast<int>(D), static_cast<int>(Dv)) : simt_attn_spec();
+    const bool simt = env_int("BFGPU_F32_SIMT", 0) == 1;
+    const bool tc = !simt && attn_f32x3_supported(D, Dv, Skv, nullptr, nullptr, nullptr, nullptr);
+    const bool tiled = !tc && attn_f32_tiled_supported(D, Dv);
+    p.spec = tc ? attn_f32x3_spec(static_cast<int>(D), static_cast<int>(Dv))
+                : tiled ? attn_f32_tiled_spec(static_cast<int>(D), static_cast<int>(Dv)) : simt_attn_spec();
     p.units = cdiv(Sq, p.spec.tile_m);
     p.tiles = p.units * BH;
     p.resident_ctas = resident_ctas(p.spec);
     p.grid = static_cast<int>(std::min<int64_t>(p.tiles, 1 << 30));
-    if (tiled)
+    if (tc)
+      why << "fp32 mode: 3xTF32 flash attention on tcgen05 (S = QK^T and O += PV each as three TF32 products, Q and P "
+             "hi/lo in TMEM, K/V blocks split in SMEM by converter warps), one CTA per (head, 128 query rows)";
+    else if (tiled)
       why << "fp32 mode: FP32 FMA flash attention, one CTA per (head, 64 query rows), key blocks of 64 in SMEM";
     else
       why << "fp32 mode: FP32 SIMT online softmax (head dims outside 64/128), one CTA per (head, 16 query rows)";

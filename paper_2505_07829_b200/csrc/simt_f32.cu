@@ -13,6 +13,8 @@
 //   K3: online-softmax attention, one CTA per (head, 16 query rows).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.hpp"
 #include "plan.hpp"
 
@@ -488,6 +490,14 @@ void lnmm_f32(const void* X, const void* Yt, void* O, int64_t M, int64_t K, int6
                                  static_cast<float*>(O), M, N, K, {1.0f / static_cast<float>(K), eps}, stream);
 }
 
+// BFGPU_F32_SIMT=1 keeps the FMA kernels (the planner reads the same variable).
+static bool f32_simt_forced() {
+  const char* v = std::getenv("BFGPU_F32_SIMT");
+  return v != nullptr && std::atoi(v) == 1;
+}
+
+void attention_f32x3(const float* Q, const float* K, const float* Vt, float* O, int64_t BH, int64_t Sq, int64_t Skv,
+                     int64_t D, int64_t Dv, float scale, cudaStream_t stream);
 void attention_f32_tiled(const float* Q, const float* K, const float* Vt, float* O, int64_t BH, int64_t Sq,
                          int64_t Skv, int64_t D, int64_t Dv, float scale, cudaStream_t stream);
 
@@ -497,6 +507,11 @@ void attention_f32(const void* Q, const void* K, const void* Vt, void* O, int64_
   BF_CHECK_ARG(D <= simt::AMAXD && Dv <= simt::AMAXD, "bf_attention: fp32 mode supports D, Dv <= 256");
   BF_CHECK_ARG(BH <= 65535, "bf_attention: too many heads for one launch");
   if (scale <= 0.f) scale = 1.0f / sqrtf(static_cast<float>(D));
+  if (!f32_simt_forced() && attn_f32x3_supported(D, Dv, Skv, Q, K, Vt, O)) {
+    attention_f32x3(static_cast<const float*>(Q), static_cast<const float*>(K), static_cast<const float*>(Vt),
+                    static_cast<float*>(O), BH, Sq, Skv, D, Dv, scale, stream);
+    return;
+  }
   if (attn_f32_tiled_supported(D, Dv)) {
     attention_f32_tiled(static_cast<const float*>(Q), static_cast<const float*>(K), static_cast<const float*>(Vt),
                         static_cast<float*>(O), BH, Sq, Skv, D, Dv, scale, stream);

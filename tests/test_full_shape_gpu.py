@@ -211,9 +211,10 @@ def test_c3_fp32_tensor_cores(torch_ops):
 
 
 def test_c2_fp32_every_head(torch_ops):
-    """K3 fp32 mode at the C2 shape (tiled FMA flash attention): every head on two query rows per
-    64-row tile vs float64 on the device, at the 1e-4 bar."""
+    """K3 fp32 mode at the C2 shape (3xTF32 flash attention on tcgen05): every head on two query
+    rows per 64-row block vs float64 on the device, at the 1e-4 bar."""
     torch, ops = torch_ops
+    assert ops.plan("attention", (256, 2048, 2048, 128, 128), dtype=torch.float32)["kernel"] == "attn_f32x3_kernel"
     g = torch.Generator(device="cuda").manual_seed(42)
     BH, S, D = 256, 2048, 128
     Q = torch.randn(BH, S, D, device="cuda", generator=g)

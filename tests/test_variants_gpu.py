@@ -2,7 +2,7 @@
 process, hence the subprocesses): the 1-SM K1 and K2 kernels (BFGPU_FFN_1SM, BFGPU_LNMM_1SM),
 the 512x256-tile K2 (BFGPU_LNMM_WIDE),
 the FMA-pipe exponential splits of K3 (BFGPU_ATTN_EMU), non-default K1/K2 scheduling groups
-(BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP) and the K1 wave sync forced on at a size where it is off by default (BFGPU_FFN_WAVESYNC=1).
+(BFGPU_FFN_GROUP, BFGPU_LNMM_GROUP), the FP32 FMA kernels of the fp32 mode (BFGPU_F32_SIMT) and the K1 wave sync forced on at a size where it is off by default (BFGPU_FFN_WAVESYNC=1).
 Same oracle and tolerances as the default-path tests."""
 import os
 import subprocess
@@ -18,7 +18,7 @@ ROOT = Path(__file__).resolve().parents[1]
 SNIPPET = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
-from helpers import assert_bf16_close, bf16_round
+from helpers import assert_bf16_close, assert_f32_close, bf16_round
 from oracle import cpu
 from paper_2505_07829_b200 import ops
 rng = np.random.default_rng(7)
@@ -36,6 +36,24 @@ elif what == "lnmm":
     X = bf16_round(rng.standard_normal((M, K)) * 3 + 1.5); Yt = bf16_round(rng.standard_normal((N, K)))
     out = ops.layernorm_matmul(t(X), t(Yt)).double().cpu().numpy()
     assert_bf16_close(out, cpu.layernorm_matmul(X, Yt), "K2 variant")
+elif what == "f32":
+    # the FP32 FMA kernels (BFGPU_F32_SIMT=1) instead of the 3xTF32 tensor-core plans
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().float()
+    assert not ops.plan("attention", (3, 300, 456, 128, 64), dtype=torch.float32)["kernel"].startswith("attn_f32x3")
+    X = rng.standard_normal((200, 136)).astype(np.float32).astype(np.float64)
+    Wt = (rng.standard_normal((264, 136)) / 12).astype(np.float32).astype(np.float64)
+    Vt = (rng.standard_normal((264, 136)) / 12).astype(np.float32).astype(np.float64)
+    Ut = (rng.standard_normal((72, 264)) / 16).astype(np.float32).astype(np.float64)
+    out = ops.rms_ffn_swiglu(f(X), f(Wt), f(Vt), f(Ut)).double().cpu().numpy()
+    assert_f32_close(out, cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 fp32 FMA")
+    Y = rng.standard_normal((96, 136)).astype(np.float32).astype(np.float64)
+    out = ops.layernorm_matmul(f(X), f(Y)).double().cpu().numpy()
+    assert_f32_close(out, cpu.layernorm_matmul(X, Y), "K2 fp32 FMA")
+    Q = rng.standard_normal((3, 300, 128)).astype(np.float32).astype(np.float64)
+    K = rng.standard_normal((3, 456, 128)).astype(np.float32).astype(np.float64)
+    Vt = rng.standard_normal((3, 64, 456)).astype(np.float32).astype(np.float64)
+    out = ops.attention(f(Q), f(K), f(Vt)).double().cpu().numpy()
+    assert_f32_close(out, cpu.attention_safe(Q, K, Vt), "K3 fp32 FMA")
 else:
     Q = bf16_round(rng.standard_normal((3, 300, 128))); K = bf16_round(rng.standard_normal((3, 456, 128)))
     Vt = bf16_round(rng.standard_normal((3, 128, 456)))
@@ -61,6 +79,7 @@ print("ok")
         ("attn", {"BFGPU_ATTN_EMU": "0"}),
         ("attn", {"BFGPU_ATTN_EMU": "12"}),
         ("attn", {"BFGPU_ATTN_EMU": "16"}),
+        ("f32", {"BFGPU_F32_SIMT": "1"}),
     ],
 )
 def test_variant_matches_oracle(what, env):
