@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "plan.hpp"
@@ -443,11 +444,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
 int64_t padded_k(int64_t K) { return (K + BK - 1) / BK * BK; }
 
-// Largest power of two of m-tiles whose hi/lo A rows (128 x Kp x 8 bytes each) fit a third of L2.
+// Tile raster group (m-tiles per group, n slow inside a group): the largest power of two whose
+// hi/lo A rows (128 x Kp x 8 bytes each) fit a third of L2, but at least 8. For long
+// contractions (K1's down GEMM, Kp = 14336) the slab never fits, and what matters is the shape
+// of one wave of 74 CTA pairs: 8 m-tiles x ~9 n-tiles read 17 operand stripes per wave where
+// 2 x 37 read 39 (16.4 -> ~7 GB of DRAM per launch at C3, ncu).
 int raster_group(int64_t Mt, int64_t Kp, int64_t l2_bytes) {
   const int64_t fit = std::max<int64_t>(1, l2_bytes / 3 / (static_cast<int64_t>(BM) * Kp * 8));
   int g = 1;
-  while (2 * g <= fit && 2 * g <= Mt) g *= 2;
+  while (2 * g <= std::max<int64_t>(fit, 8) && 2 * g <= Mt) g *= 2;
+  if (const char* e = std::getenv("BFGPU_F32_GROUP")) g = std::max(1, std::atoi(e));
   return g;
 }
 
