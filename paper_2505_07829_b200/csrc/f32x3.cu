@@ -49,12 +49,13 @@ constexpr int NUM_THREADS = 256;
 // kind::tf32 instruction descriptor: D F32, A/B TF32 (format 2), both K-major, N/8, M/16
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
 
-__device__ __forceinline__ void umma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void umma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate,
+                                             uint32_t idesc = IDESC) {
   asm volatile(
       "{\n.reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate)
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
@@ -190,11 +191,17 @@ __global__ void __launch_bounds__(256) f32_split_kernel(const __grid_constant__ 
 //   kPlain  O = acc                                                        (K1, down)
 enum Mode { kLn = 0, kGate = 1, kPlain = 2 };
 
-template <int MODE>
+// BNT: output tile width. 128 everywhere; 256 for kLn/kPlain launches with enough tiles (one
+// N = 256 MMA reads 12 KB of SMEM per 128 tensor cycles where two N = 128 MMAs read 16 KB, and
+// these kernels are bound by SMEM bandwidth: DESIGN.md, K2 fp32).
+template <int MODE, int BNT = 128>
 struct GCfg {
+  static constexpr int BN = BNT;
+  static constexpr int B_BYTES = BNT * BK * 4;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((BNT >> 3) << 17) | ((BM >> 4) << 24);
   static constexpr int NB = MODE == kGate ? 2 : 1;  // B operands sharing the A tile
   static constexpr int STAGE_BYTES = 2 * A_BYTES + NB * 2 * B_BYTES;
-  static constexpr int STAGES = MODE == kGate ? 2 : 3;
+  static constexpr int STAGES = STAGE_BYTES > 64 * 1024 ? 2 : 3;
   static constexpr uint32_t TMEM_COLS = NB * BN;
   static constexpr int RED_PITCH = NB * (BN / 2) * 4 + 16;  // pushed-half row pitch (bytes): rows on distinct banks
   static_assert(BM * RED_PITCH <= STAGES * STAGE_BYTES, "reduction buffer reuses the operand ring");
@@ -213,14 +220,15 @@ struct GemmParams {
   float* O2;  // kGate: h_lo
 };
 
-template <int MODE>
+template <int MODE, int BNT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     f32x3_gemm_kernel(const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
                       const __grid_constant__ CUtensorMap tm_yh, const __grid_constant__ CUtensorMap tm_yl,
                       const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_vl,
                       const GemmParams p) {
   using namespace dev;
-  using C = GCfg<MODE>;
+  using C = GCfg<MODE, BNT>;
+  constexpr int BN = C::BN, B_BYTES = C::B_BYTES;  // this instantiation's tile width
   extern __shared__ __align__(1024) uint8_t smem[];
   if (smem_u32(smem) & 1023u) __trap();
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -298,9 +306,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #endif
             const uint32_t o = kk * 32;
             // small terms first: lo*hi, hi*lo, then hi*hi
-            umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0);
-            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1);
-            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0, C::IDESC);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1, C::IDESC);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1, C::IDESC);
           }
         }
         umma_commit(&empty[s]);
@@ -314,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   // tile. Each rank pushes its partial sums of the other half into the peer's SMEM (remote
   // stores: no round-trip latency exposed), then adds the peer's pushed half to its own TMEM
   // half in a fixed order (deterministic). The rings are free once both pairs' MMAs are done.
-  constexpr int HALF = BN / 2;
+  constexpr int HALF = BN / 2, CH = HALF / 32;  // columns per rank, 32-column chunks per half
   const uint32_t q = warp & 3;
   const uint32_t trow = q * 32 + lane;
   const uint32_t tl = tmem + ((q * 32) << 16);
@@ -328,8 +336,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp >= 4) {
     const uint32_t dst = mapa_shared(smem_u32(red), rank ^ 1);
 #pragma unroll 1
-    for (int c = 0; c < C::NB * 2; ++c) {  // (operand b, 32-column chunk) of the peer's half
-      const int b = c >> 1, col = b * BN + static_cast<int>(rank ^ 1) * HALF + (c & 1) * 32;
+    for (int c = 0; c < C::NB * CH; ++c) {  // (operand b, 32-column chunk) of the peer's half
+      const int b = c / CH, col = b * BN + static_cast<int>(rank ^ 1) * HALF + (c % CH) * 32;
       uint32_t v[32];
       tmem_ld_32x32b_x32(tl + col, v);
       tmem_wait_ld();
@@ -338,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const float4 f = nk > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
                                               __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        st_cluster_v4(dst + (b * HALF + (c & 1) * 32 + 4 * i) * 4, f);
+        st_cluster_v4(dst + (b * HALF + (c % CH) * 32 + 4 * i) * 4, f);
       }
     }
   }
@@ -356,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (p.M > 0) goto epi_done;
 #endif
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < CH; ++c) {
       const int cbase = static_cast<int>(rank) * HALF + c * 32;  // tile column of this chunk
       uint32_t v[32];
       tmem_ld_32x32b_x32(tl + cbase, v);
@@ -403,11 +411,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
     __syncwarp();
-    // the warp's 32 rows x 64 columns, two rows per instruction (256 contiguous bytes each)
+    // the warp's 32 rows x HALF columns, RPI rows per instruction (HALF * 4 contiguous bytes each)
+    constexpr int LPR = HALF / 4, RPI = 32 / LPR;  // lanes per row, rows per instruction
 #pragma unroll 4
-    for (int k = 0; k < 16; ++k) {
-      const int cc = (lane & 15) * 4, col = n0 + static_cast<int>(rank) * HALF + cc;
-      const int rl = 2 * k + static_cast<int>(lane >> 4), row2 = m0 + static_cast<int>(q) * 32 + rl;
+    for (int k = 0; k < 32 / RPI; ++k) {
+      const int cc = (static_cast<int>(lane) % LPR) * 4, col = n0 + static_cast<int>(rank) * HALF + cc;
+      const int rl = RPI * k + static_cast<int>(lane) / LPR, row2 = m0 + static_cast<int>(q) * 32 + rl;
       if (row2 >= p.M) break;
       const uint8_t* srow = smem + (q * 32 + rl) * C::RED_PITCH;
       const float4 val = *reinterpret_cast<const float4*>(srow + cc * 4);
@@ -457,10 +466,10 @@ int raster_group(int64_t Mt, int64_t Kp, int64_t l2_bytes) {
   return g;
 }
 
-template <int MODE>
+template <int MODE, int BNT = 128>
 void launch_gemm(const CUtensorMap (&tm)[6], const GemmParams& gp, cudaStream_t stream) {
-  using C = GCfg<MODE>;
-  ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_gemm_kernel<MODE>), C::SMEM);
+  using C = GCfg<MODE, BNT>;
+  ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_gemm_kernel<MODE, BNT>), C::SMEM);
   const int64_t tiles = static_cast<int64_t>(gp.Mt) * gp.Nt;
   BF_CHECK_ARG(2 * tiles < (1ll << 31), "fp32 mode: too many output tiles for one launch");
   // launched as a programmatic dependent of the previous launch (griddepcontrol in both)
@@ -474,7 +483,7 @@ void launch_gemm(const CUtensorMap (&tm)[6], const GemmParams& gp, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel<MODE>, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], gp));
+  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel<MODE, BNT>, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], gp));
   note_launch();
 }
 
@@ -514,7 +523,13 @@ size_t ffn_f32x3_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
   return 2 * a(M * dp) + 4 * a(F * dp) + 2 * a(N * fp) + 2 * a(M * fp) + a(M);
 }
 
-KernelSpec f32x3_gemm_spec(int mode) {
+// 128 x 256 tiles when there are enough of them: at least one per SM (CTA pairs x 2).
+bool f32x3_wide(int64_t M, int64_t N) {
+  if (const char* e = std::getenv("BFGPU_F32_BN")) return std::atoi(e) == 256;
+  return ((M + f32x3::BM - 1) / f32x3::BM) * ((N + 255) / 256) >= 148;
+}
+
+KernelSpec f32x3_gemm_spec(int mode, bool wide) {
   using namespace f32x3;
   KernelSpec k;
   k.threads = NUM_THREADS;
@@ -532,14 +547,21 @@ KernelSpec f32x3_gemm_spec(int mode) {
   };
   if (mode == kGate) {
     k.name = "f32x3_gemm_kernel<gate>";
-    fill(GCfg<kGate>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kGate>));
+    fill(GCfg<kGate>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kGate, 128>));
+  } else if (mode == kPlain && wide) {
+    k.name = "f32x3_gemm_kernel<plain,256>";
+    fill(GCfg<kPlain, 256>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kPlain, 256>));
   } else if (mode == kPlain) {
     k.name = "f32x3_gemm_kernel<plain>";
-    fill(GCfg<kPlain>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kPlain>));
+    fill(GCfg<kPlain>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kPlain, 128>));
+  } else if (wide) {
+    k.name = "f32x3_gemm_kernel<ln,256>";
+    fill(GCfg<kLn, 256>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kLn, 256>));
   } else {
     k.name = "f32x3_gemm_kernel";
-    fill(GCfg<kLn>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kLn>));
+    fill(GCfg<kLn>{}, reinterpret_cast<const void*>(&f32x3_gemm_kernel<kLn, 128>));
   }
+  if (wide && mode != kGate) k.tile_n = 256;
   return k;
 }
 
@@ -565,21 +587,26 @@ void lnmm_f32x3(const Plan& pl, const void* X, const void* Yt, void* O, float ep
   sp.eps = eps;
   launch_split(sp, pl.dev.sms, stream);
 
-  const CUtensorMap tm[6] = {tmap(xh, M, Kp, BM), tmap(xl, M, Kp, BM), tmap(yh, N, Kp, BN),
-                             tmap(yl, N, Kp, BN), tmap(yh, N, Kp, BN), tmap(yl, N, Kp, BN)};
+  const bool wide = f32x3_wide(M, N);
+  const int bn = wide ? 256 : BN;
+  const CUtensorMap tm[6] = {tmap(xh, M, Kp, BM), tmap(xl, M, Kp, BM), tmap(yh, N, Kp, bn),
+                             tmap(yl, N, Kp, bn), tmap(yh, N, Kp, bn), tmap(yl, N, Kp, bn)};
   GemmParams gp{};
   gp.M = static_cast<int>(M);
   gp.N = static_cast<int>(N);
   gp.ldo = static_cast<int>(N);
   gp.kt = static_cast<int>(Kp / BK);
   gp.Mt = static_cast<int>((M + BM - 1) / BM);
-  gp.Nt = static_cast<int>((N + BN - 1) / BN);
+  gp.Nt = static_cast<int>((N + bn - 1) / bn);
   gp.group = raster_group(gp.Mt, Kp, pl.dev.l2_bytes);
   gp.rstd = rstd;
   gp.negdm = negdm;
   gp.colsum = colsum;
   gp.O = static_cast<float*>(O);
-  launch_gemm<kLn>(tm, gp, stream);
+  if (wide)
+    launch_gemm<kLn, 256>(tm, gp, stream);
+  else
+    launch_gemm<kLn>(tm, gp, stream);
 }
 
 // K1 fp32 mode on the tensor cores: split {X (RMSNorm rows), Wt, Vt, Ut}, then the gate/up GEMM
@@ -625,18 +652,23 @@ void ffn_f32x3(const Plan& pl, const void* X, const void* Wt, const void* Vt, co
   g1.O2 = hl;
   launch_gemm<kGate>(tg, g1, stream);
 
-  const CUtensorMap td[6] = {tmap(hh, M, Fp, BM), tmap(hl, M, Fp, BM), tmap(uh, N, Fp, BN),
-                             tmap(ul, N, Fp, BN), tmap(uh, N, Fp, BN), tmap(ul, N, Fp, BN)};
+  const bool wide = f32x3_wide(M, N);
+  const int bn = wide ? 256 : BN;
+  const CUtensorMap td[6] = {tmap(hh, M, Fp, BM), tmap(hl, M, Fp, BM), tmap(uh, N, Fp, bn),
+                             tmap(ul, N, Fp, bn), tmap(uh, N, Fp, bn), tmap(ul, N, Fp, bn)};
   GemmParams g2{};
   g2.M = m;
   g2.N = n;
   g2.ldo = n;
   g2.kt = static_cast<int>(Fp / BK);
   g2.Mt = g1.Mt;
-  g2.Nt = static_cast<int>((N + BN - 1) / BN);
+  g2.Nt = static_cast<int>((N + bn - 1) / bn);
   g2.group = raster_group(g2.Mt, Fp, pl.dev.l2_bytes);
   g2.O = static_cast<float*>(O);
-  launch_gemm<kPlain>(td, g2, stream);
+  if (wide)
+    launch_gemm<kPlain, 256>(td, g2, stream);
+  else
+    launch_gemm<kPlain>(td, g2, stream);
 }
 
 }  // namespace bfgpu

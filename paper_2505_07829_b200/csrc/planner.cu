@@ -275,7 +275,7 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int sched
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
     const bool simt = env_int("BFGPU_F32_SIMT", 0) == 1;
-    p.spec = simt ? simt_gemm_spec(2) : f32x3_gemm_spec();
+    p.spec = simt ? simt_gemm_spec(2) : f32x3_gemm_spec(0, f32x3_wide(M, N));
     p.units = cdiv(M, p.spec.tile_m);
     p.tiles = p.units * cdiv(N, p.spec.tile_n);
     p.resident_ctas = resident_ctas(p.spec);
@@ -286,7 +286,7 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int sched
       why << "fp32 mode: 3xTF32 on tcgen05 (x = hi + lo, hi*hi + hi*lo + lo*hi in the fp32 TMEM accumulator, "
              "~1e-6 relative at K=1024, inside the 1e-4 bar that one TF32 pass misses); a split launch computes "
              "the row statistics and colsum(Yt) and writes pivot-shifted hi/lo operands (" << 8.0 * (M + N) * ((K + 31) / 32 * 32) / 1e6
-          << " MB), then " << p.tiles << " 128x128 tiles, each with its K range split over a CTA pair "
+          << " MB), then " << p.tiles << " 128x" << p.spec.tile_n << " tiles, each with its K range split over a CTA pair "
              "(DSMEM reduction), on a 3-stage TMA ring";
     (void)schedule;
     p.notes = why.str();
