@@ -19,6 +19,11 @@ for s in ("fused", "staged"):
     ops.attention(Q, K, Vv, schedule=s)
 ops.attention(Q.float(), K.float(), Vv.float())
 ops.rms_ffn_swiglu(X.float(), Wt.float(), Vt.float(), Ut.float())
+import os
+os.environ["BFGPU_F32_BN"] = "256"  # the 128x256-tile 3xTF32 GEMMs at a small shape
+ops.layernorm_matmul(Xl.float(), Yt.float())
+ops.rms_ffn_swiglu(X.float(), Wt.float(), Vt.float(), Ut.float())
+ops.attention(Q.float()[:, :, :64].contiguous(), K.float()[:, :, :64].contiguous(), Vv.float()[:, :64].contiguous())
 torch.cuda.synchronize()
 print("san ok")
 PY
