@@ -451,6 +451,181 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant for large launches: 256 x 256 output tiles, M = 256 cta_group::2 MMAs
+// issued by the pair leader. Each CTA stages its own 128 rows of A and 128 rows of B (hi and
+// lo), so per K step a CTA writes 64 KB and its SMEM serves 96 KB to the MMAs for 4x the
+// FLOPs of a 128 x 128 step (which moves 160 KB): the pair kernel is no longer bound by SMEM
+// bandwidth. No K split: each CTA finalizes its own 128 rows x 256 columns. Even and odd K
+// steps accumulate into two TMEM accumulators (512 columns), added once in the epilogue: the
+// tensor core's accumulation is not round-to-nearest fp32, and one accumulator over K = 14336
+// (K1's down GEMM at C3) measured 1.46e-4 against float64, over the 1e-4 bar; two halve the
+// chain, as the K split of the single-CTA kernel does.
+constexpr int P2_BN = 256, P2_STAGES = 3;
+constexpr int P2_STAGE_BYTES = 2 * A_BYTES + 2 * (128 * BK * 4);  // X_hi | X_lo | Y_hi | Y_lo (this CTA's halves)
+constexpr int P2_OUT_PITCH = P2_BN * 4 + 16;
+static_assert(BM * P2_OUT_PITCH <= P2_STAGES * P2_STAGE_BYTES, "output staging reuses the operand ring");
+constexpr int P2_SMEM = P2_STAGES * P2_STAGE_BYTES + 256;
+constexpr uint32_t P2_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((P2_BN >> 3) << 17) | ((256 >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32_ss_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(P2_IDESC), "r"(accumulate)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    f32x3_pair_kernel(const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
+                      const __grid_constant__ CUtensorMap tm_yh, const __grid_constant__ CUtensorMap tm_yl,
+                      const GemmParams p) {
+  static_assert(MODE == kLn || MODE == kPlain, "pair kernel epilogues");
+  using namespace dev;
+  constexpr int Y_BYTES = 128 * BK * 4;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (smem_u32(smem) & 1023u) __trap();
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P2_STAGES * P2_STAGE_BYTES);
+  uint64_t* empty = full + P2_STAGES;
+  uint64_t* tfull = empty + P2_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  // grouped raster over 256 x 256 tiles
+  const int t = static_cast<int>(blockIdx.x >> 1);
+  const int per_group = p.group * p.Nt, g = t / per_group, in_g = t % per_group;
+  const int gm = min(p.group, p.Mt - g * p.group);
+  const int m0 = (g * p.group + in_g % gm) * 256, n0 = (in_g / gm) * P2_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_xh);
+    tma_prefetch_desc(&tm_xl);
+    tma_prefetch_desc(&tm_yh);
+    tma_prefetch_desc(&tm_yl);
+    for (int s = 0; s < P2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<2 * P2_BN>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+      const int arow = m0 + static_cast<int>(rank) * 128, brow = n0 + static_cast<int>(rank) * 128;
+      for (int i = 0; i < p.kt; ++i) {
+        const int s = i % P2_STAGES;
+        mbar_wait(&empty[s], ((i / P2_STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * P2_STAGE_BYTES;
+        const uint32_t fbar = full0 + s * 8;
+        if (leader) mbar_arrive_expect_tx(&full[s], 2 * P2_STAGE_BYTES);
+        tma_load_2d_2sm(&tm_xh, fbar, st, i * BK, arow);
+        tma_load_2d_2sm(&tm_xl, fbar, st + A_BYTES, i * BK, arow);
+        tma_load_2d_2sm(&tm_yh, fbar, st + 2 * A_BYTES, i * BK, brow);
+        tma_load_2d_2sm(&tm_yl, fbar, st + 2 * A_BYTES + Y_BYTES, i * BK, brow);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      for (int i = 0; i < p.kt; ++i) {
+        const int s = i % P2_STAGES;
+        mbar_wait(&full[s], (i / P2_STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t xh = smem_u32(smem + s * P2_STAGE_BYTES), xl = xh + A_BYTES, yh = xh + 2 * A_BYTES,
+                         yl = yh + Y_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t o = kk * 32;
+            const uint32_t d = tmem + (i & 1) * P2_BN;  // even / odd K steps
+            umma_tf32_ss_2sm(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i >= 2 || kk != 0));
+            umma_tf32_ss_2sm(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1);
+            umma_tf32_ss_2sm(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1);
+          }
+          umma_commit_2sm_mc(&empty[s], 0x3);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) umma_commit_2sm_mc(tfull, 0x3);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: this CTA's 128 rows x 256 columns, staged in the idle ring, stored coalesced
+    const uint32_t q = warp & 3;
+    const uint32_t trow = q * 32 + lane;
+    const uint32_t tl = tmem + ((q * 32) << 16);
+    const int row = m0 + static_cast<int>(rank) * 128 + static_cast<int>(trow);
+    float r = 1.f, nd = 0.f;
+    if constexpr (MODE == kLn) {
+      r = row < p.M ? __ldg(p.rstd + row) : 0.f;
+      nd = row < p.M ? __ldg(p.negdm + row) : 0.f;
+    }
+    mbar_wait(tfull, 0);  // all MMAs of the pair done: both operand rings are idle
+    tc_fence_after();
+    float4* srow = reinterpret_cast<float4*>(smem + trow * P2_OUT_PITCH);
+#pragma unroll 1
+    for (int c = 0; c < P2_BN / 32; ++c) {
+      uint32_t v[32], w[32];
+      tmem_ld_32x32b_x32(tl + c * 32, v);
+      tmem_ld_32x32b_x32(tl + P2_BN + c * 32, w);
+      tmem_wait_ld();
+      const bool two = p.kt > 1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float a = two ? __uint_as_float(v[4 * i + u]) + __uint_as_float(w[4 * i + u])
+                              : __uint_as_float(v[4 * i + u]);
+          if constexpr (MODE == kLn) {
+            const int col = n0 + c * 32 + 4 * i + u;
+            o[u] = col < p.N ? fmaf(nd, __ldg(p.colsum + col), a) * r : 0.f;
+          } else {
+            o[u] = a;
+          }
+        }
+        srow[c * 8 + i] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    __syncwarp();
+    const bool vec = (p.N & 3) == 0 && (p.ldo & 3) == 0;
+    const int rbase = m0 + static_cast<int>(rank) * 128 + static_cast<int>(q) * 32;
+#pragma unroll 4
+    for (int k = 0; k < 64; ++k) {  // 32 rows x 2 halves of 128 columns, 512 contiguous bytes each
+      const int rl = k >> 1, row2 = rbase + rl;
+      if (row2 >= p.M) break;
+      const int cc = (k & 1) * 128 + static_cast<int>(lane) * 4, col = n0 + cc;
+      const float4 val = *reinterpret_cast<const float4*>(smem + (q * 32 + rl) * P2_OUT_PITCH + cc * 4);
+      float* out = p.O + static_cast<size_t>(row2) * p.ldo + col;
+      if (vec && col + 3 < p.N) {
+        *reinterpret_cast<float4*>(out) = val;
+      } else {
+        const float e[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (col + u < p.N) out[u] = e[u];
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the leader's MMAs read this CTA's SMEM: keep both alive until the end
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<2 * P2_BN>(tmem);
+  }
+}
+
 int64_t padded_k(int64_t K) { return (K + BK - 1) / BK * BK; }
 
 // Tile raster group (m-tiles per group, n slow inside a group): the largest power of two whose
@@ -484,6 +659,25 @@ void launch_gemm(const CUtensorMap (&tm)[6], const GemmParams& gp, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_gemm_kernel<MODE, BNT>, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], gp));
+  note_launch();
+}
+
+template <int MODE>
+void launch_pair(const CUtensorMap (&tm)[6], const GemmParams& gp, cudaStream_t stream) {
+  ensure_smem_attr(reinterpret_cast<const void*>(&f32x3_pair_kernel<MODE>), P2_SMEM);
+  const int64_t tiles = static_cast<int64_t>(gp.Mt) * gp.Nt;
+  BF_CHECK_ARG(2 * tiles < (1ll << 31), "fp32 mode: too many output tiles for one launch");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * tiles));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = P2_SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, f32x3_pair_kernel<MODE>, tm[0], tm[1], tm[2], tm[3], gp));
   note_launch();
 }
 
@@ -523,10 +717,35 @@ size_t ffn_f32x3_workspace_bytes(int64_t M, int64_t D, int64_t F, int64_t N) {
   return 2 * a(M * dp) + 4 * a(F * dp) + 2 * a(N * fp) + 2 * a(M * fp) + a(M);
 }
 
+// 256 x 256 CTA-pair tiles (M = 256 MMAs, no K split) when there are at least two waves of
+// them; BFGPU_F32_PAIR=0/1 forces.
+bool f32x3_pair(int64_t M, int64_t N) {
+  if (const char* e = std::getenv("BFGPU_F32_PAIR")) return std::atoi(e) == 1;
+  return ((M + 255) / 256) * ((N + 255) / 256) >= 148;
+}
+
 // 128 x 256 tiles when there are enough of them: at least one per SM (CTA pairs x 2).
 bool f32x3_wide(int64_t M, int64_t N) {
   if (const char* e = std::getenv("BFGPU_F32_BN")) return std::atoi(e) == 256;
   return ((M + f32x3::BM - 1) / f32x3::BM) * ((N + 255) / 256) >= 148;
+}
+
+KernelSpec f32x3_pair_spec(int mode) {
+  using namespace f32x3;
+  KernelSpec k;
+  k.name = mode == kPlain ? "f32x3_pair_kernel<plain>" : "f32x3_pair_kernel<ln>";
+  k.func = mode == kPlain ? reinterpret_cast<const void*>(&f32x3_pair_kernel<kPlain>)
+                          : reinterpret_cast<const void*>(&f32x3_pair_kernel<kLn>);
+  k.threads = NUM_THREADS;
+  k.cluster = 2;  // M = 256 cta_group::2 MMAs
+  k.tile_m = 256;
+  k.tile_n = P2_BN;
+  k.tile_k = BK;
+  k.smem_bytes = P2_SMEM;
+  k.tmem_cols = 2 * P2_BN;
+  k.stages = P2_STAGES;
+  k.grid_sync = false;
+  return k;
 }
 
 KernelSpec f32x3_gemm_spec(int mode, bool wide) {
@@ -587,6 +806,24 @@ void lnmm_f32x3(const Plan& pl, const void* X, const void* Yt, void* O, float ep
   sp.eps = eps;
   launch_split(sp, pl.dev.sms, stream);
 
+  if (f32x3_pair(M, N)) {
+    const CUtensorMap tp[6] = {tmap(xh, M, Kp, BM), tmap(xl, M, Kp, BM), tmap(yh, N, Kp, 128),
+                               tmap(yl, N, Kp, 128), tmap(yh, N, Kp, 128), tmap(yl, N, Kp, 128)};
+    GemmParams gp{};
+    gp.M = static_cast<int>(M);
+    gp.N = static_cast<int>(N);
+    gp.ldo = static_cast<int>(N);
+    gp.kt = static_cast<int>(Kp / BK);
+    gp.Mt = static_cast<int>((M + 255) / 256);
+    gp.Nt = static_cast<int>((N + 255) / 256);
+    gp.group = raster_group(gp.Mt, 2 * Kp, pl.dev.l2_bytes);
+    gp.rstd = rstd;
+    gp.negdm = negdm;
+    gp.colsum = colsum;
+    gp.O = static_cast<float*>(O);
+    launch_pair<kLn>(tp, gp, stream);
+    return;
+  }
   const bool wide = f32x3_wide(M, N);
   const int bn = wide ? 256 : BN;
   const CUtensorMap tm[6] = {tmap(xh, M, Kp, BM), tmap(xl, M, Kp, BM), tmap(yh, N, Kp, bn),
@@ -652,6 +889,21 @@ void ffn_f32x3(const Plan& pl, const void* X, const void* Wt, const void* Vt, co
   g1.O2 = hl;
   launch_gemm<kGate>(tg, g1, stream);
 
+  if (f32x3_pair(M, N)) {
+    const CUtensorMap tp[6] = {tmap(hh, M, Fp, BM), tmap(hl, M, Fp, BM), tmap(uh, N, Fp, 128),
+                               tmap(ul, N, Fp, 128), tmap(uh, N, Fp, 128), tmap(ul, N, Fp, 128)};
+    GemmParams g2{};
+    g2.M = m;
+    g2.N = n;
+    g2.ldo = n;
+    g2.kt = static_cast<int>(Fp / BK);
+    g2.Mt = static_cast<int>((M + 255) / 256);
+    g2.Nt = static_cast<int>((N + 255) / 256);
+    g2.group = raster_group(g2.Mt, 2 * Fp, pl.dev.l2_bytes);
+    g2.O = static_cast<float*>(O);
+    launch_pair<kPlain>(tp, g2, stream);
+    return;
+  }
   const bool wide = f32x3_wide(M, N);
   const int bn = wide ? 256 : BN;
   const CUtensorMap td[6] = {tmap(hh, M, Fp, BM), tmap(hl, M, Fp, BM), tmap(uh, N, Fp, bn),

@@ -275,7 +275,7 @@ static Plan make_plan_lnmm(int64_t M, int64_t K, int64_t N, int dtype, int sched
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
     const bool simt = env_int("BFGPU_F32_SIMT", 0) == 1;
-    p.spec = simt ? simt_gemm_spec(2) : f32x3_gemm_spec(0, f32x3_wide(M, N));
+    p.spec = simt ? simt_gemm_spec(2) : f32x3_pair(M, N) ? f32x3_pair_spec(0) : f32x3_gemm_spec(0, f32x3_wide(M, N));
     p.units = cdiv(M, p.spec.tile_m);
     p.tiles = p.units * cdiv(N, p.spec.tile_n);
     p.resident_ctas = resident_ctas(p.spec);

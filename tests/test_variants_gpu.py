@@ -36,6 +36,20 @@ elif what == "lnmm":
     X = bf16_round(rng.standard_normal((M, K)) * 3 + 1.5); Yt = bf16_round(rng.standard_normal((N, K)))
     out = ops.layernorm_matmul(t(X), t(Yt)).double().cpu().numpy()
     assert_bf16_close(out, cpu.layernorm_matmul(X, Yt), "K2 variant")
+elif what == "f32pair":
+    # the CTA-pair 3xTF32 GEMMs (256 x 256 tiles, M = 256 MMAs) forced at ragged small shapes
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().float()
+    assert ops.plan("layernorm_matmul", (600, 264, 392), dtype=torch.float32)["kernel"].startswith("f32x3_pair")
+    X = (rng.standard_normal((600, 264)) * 2 + 3).astype(np.float32).astype(np.float64)
+    Y = rng.standard_normal((392, 264)).astype(np.float32).astype(np.float64)
+    out = ops.layernorm_matmul(f(X), f(Y)).double().cpu().numpy()
+    assert_f32_close(out, cpu.layernorm_matmul(X, Y), "K2 fp32 pair")
+    X = rng.standard_normal((300, 136)).astype(np.float32).astype(np.float64)
+    Wt = (rng.standard_normal((264, 136)) / 12).astype(np.float32).astype(np.float64)
+    Vt = (rng.standard_normal((264, 136)) / 12).astype(np.float32).astype(np.float64)
+    Ut = (rng.standard_normal((328, 264)) / 16).astype(np.float32).astype(np.float64)
+    out = ops.rms_ffn_swiglu(f(X), f(Wt), f(Vt), f(Ut)).double().cpu().numpy()
+    assert_f32_close(out, cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 fp32 pair down GEMM")
 elif what == "f32":
     # the FP32 FMA kernels (BFGPU_F32_SIMT=1) instead of the 3xTF32 tensor-core plans
     f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().float()
@@ -80,6 +94,8 @@ print("ok")
         ("attn", {"BFGPU_ATTN_EMU": "12"}),
         ("attn", {"BFGPU_ATTN_EMU": "16"}),
         ("f32", {"BFGPU_F32_SIMT": "1"}),
+        ("f32pair", {"BFGPU_F32_PAIR": "1"}),
+        ("f32pair", {"BFGPU_F32_PAIR": "1", "BFGPU_F32_GROUP": "1"}),
     ],
 )
 def test_variant_matches_oracle(what, env):
