@@ -202,7 +202,11 @@ struct GCfg {
   static constexpr int NB = MODE == kGate ? 2 : 1;  // B operands sharing the A tile
   static constexpr int STAGE_BYTES = 2 * A_BYTES + NB * 2 * B_BYTES;
   static constexpr int STAGES = STAGE_BYTES > 64 * 1024 ? 2 : 3;
-  static constexpr uint32_t TMEM_COLS = NB * BN;
+  // even and odd K steps accumulate into separate sets (added in the epilogue): the tensor
+  // core's accumulation is not round-to-nearest, and halving each chain keeps K1's fp32 mode
+  // (two chained contractions) clear of the 1e-4 bar
+  static constexpr int SET = NB * BN;
+  static constexpr uint32_t TMEM_COLS = 2 * SET;
   static constexpr int RED_PITCH = NB * (BN / 2) * 4 + 16;  // pushed-half row pitch (bytes): rows on distinct banks
   static_assert(BM * RED_PITCH <= STAGES * STAGE_BYTES, "reduction buffer reuses the operand ring");
   static constexpr int SMEM = STAGES * STAGE_BYTES + 256;
@@ -298,7 +302,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t xh = smem_u32(smem + s * C::STAGE_BYTES), xl = xh + A_BYTES;
 #pragma unroll
         for (int b = 0; b < C::NB; ++b) {
-          const uint32_t yh = xh + 2 * A_BYTES + 2 * b * B_BYTES, yl = yh + B_BYTES, d = tmem + b * BN;
+          const uint32_t yh = xh + 2 * A_BYTES + 2 * b * B_BYTES, yl = yh + B_BYTES,
+                         d = tmem + (i & 1) * C::SET + b * BN;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 = 32 bytes per MMA
 #ifdef BF_F32X3_DBG_NOMMA  // timing only: the load pipeline alone
@@ -306,7 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #endif
             const uint32_t o = kk * 32;
             // small terms first: lo*hi, hi*lo, then hi*hi
-            umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i | kk) != 0, C::IDESC);
+            umma_tf32_ss(d, sdesc_kmajor_sw128(xl + o), sdesc_kmajor_sw128(yh + o), (i >= 2 || kk != 0), C::IDESC);
             umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yl + o), 1, C::IDESC);
             umma_tf32_ss(d, sdesc_kmajor_sw128(xh + o), sdesc_kmajor_sw128(yh + o), 1, C::IDESC);
           }
@@ -338,14 +343,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
     for (int c = 0; c < C::NB * CH; ++c) {  // (operand b, 32-column chunk) of the peer's half
       const int b = c / CH, col = b * BN + static_cast<int>(rank ^ 1) * HALF + (c % CH) * 32;
-      uint32_t v[32];
+      uint32_t v[32], v2[32];
       tmem_ld_32x32b_x32(tl + col, v);
+      tmem_ld_32x32b_x32(tl + C::SET + col, v2);
       tmem_wait_ld();
+      const bool two = nk > 1;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float4 f = nk > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        float e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          e[u] = nk == 0 ? 0.f
+                         : (two ? __uint_as_float(v[4 * i + u]) + __uint_as_float(v2[4 * i + u])
+                                : __uint_as_float(v[4 * i + u]));
+        const float4 f = make_float4(e[0], e[1], e[2], e[3]);
         st_cluster_v4(dst + (b * HALF + (c % CH) * 32 + 4 * i) * 4, f);
       }
     }
@@ -366,13 +377,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
       const int cbase = static_cast<int>(rank) * HALF + c * 32;  // tile column of this chunk
-      uint32_t v[32];
+      uint32_t v[32], v2[32];
       tmem_ld_32x32b_x32(tl + cbase, v);
-      uint32_t w[32];
-      if constexpr (C::NB == 2) tmem_ld_32x32b_x32(tl + BN + cbase, w);
+      tmem_ld_32x32b_x32(tl + C::SET + cbase, v2);
+      uint32_t w[32], w2[32];
+      if constexpr (C::NB == 2) {
+        tmem_ld_32x32b_x32(tl + BN + cbase, w);
+        tmem_ld_32x32b_x32(tl + C::SET + BN + cbase, w2);
+      }
       tmem_wait_ld();
       if (row >= p.M) continue;
       const bool own = nk > 0;
+      if (nk > 1) {  // fold the odd-step set into the even one (round-to-nearest fp32 adds)
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          v[u] = __float_as_uint(__uint_as_float(v[u]) + __uint_as_float(v2[u]));
+          if constexpr (C::NB == 2) w[u] = __float_as_uint(__uint_as_float(w[u]) + __uint_as_float(w2[u]));
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int col = n0 + cbase + 4 * i;

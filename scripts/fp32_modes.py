@@ -25,10 +25,22 @@ M, D, F = 8192, 4096, 14336
 X, Wt, Vt, Ut = r(M, D), r(F, D) * D ** -0.5, r(F, D) * D ** -0.5, r(D, F) * F ** -0.5
 ms = t(lambda: ops.rms_ffn_swiglu(X, Wt, Vt, Ut))
 print(f"K1 fp32 C3: {ms:.2f} ms {6 * M * D * F / ms / 1e9:.1f} TFLOP/s")
+rows = torch.arange(0, M, 97, device="cuda")
+Xr = X[rows].double()
+Xn = Xr * torch.rsqrt(Xr.pow(2).mean(-1, keepdim=True))
+a, b = Xn @ Wt.double().T, Xn @ Vt.double().T
+ref = (a * torch.sigmoid(a) * b) @ Ut.double().T
+O = ops.rms_ffn_swiglu(X, Wt, Vt, Ut)[rows].double()
+print(f"K1 fp32 C3 {rows.numel()} rows: max|d|/max|ref| = {float((O - ref).abs().max() / ref.abs().max()):.2e}")
 del X, Wt, Vt, Ut
 X, Yt = r(65536, 4096), r(4096, 4096)
 ms = t(lambda: ops.layernorm_matmul(X, Yt))
 print(f"K2 fp32 C4: {ms:.2f} ms {2 * 65536 * 4096 * 4096 / ms / 1e9:.1f} TFLOP/s")
+rows = torch.arange(0, 65536, 811, device="cuda")
+Xr = X[rows].double()
+ref = ((Xr - Xr.mean(-1, keepdim=True)) / Xr.std(-1, unbiased=False, keepdim=True)) @ Yt.double().T
+O = ops.layernorm_matmul(X, Yt)[rows].double()
+print(f"K2 fp32 C4 {rows.numel()} rows: max|d|/max|ref| = {float((O - ref).abs().max() / ref.abs().max()):.2e}")
 del X, Yt
 Q, K, V = r(256, 2048, 128), r(256, 2048, 128), r(256, 128, 2048)
 ms = t(lambda: ops.attention(Q, K, V))
