@@ -19,6 +19,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:f32 -s 4 -c 2 -o $O/prof_c1 -f python scripts/ncu_target.py lnmm_c1 fused 3 > $O/ncu_c1.log 2>&1
 ls -la $O
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_f32x3 -s 1 -c 1 -o $O/prof_attn_f32 -f python scripts/ncu_fp32_target.py attn > $O/ncu_attn_f32.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:f32x3_gemm -s 2 -c 2 -o $O/prof_ffn_f32 -f python scripts/ncu_fp32_target.py ffn > $O/ncu_ffn_f32.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"f32x3_(gemm|pair)" -s 2 -c 2 -o $O/prof_ffn_f32 -f python scripts/ncu_fp32_target.py ffn > $O/ncu_ffn_f32.log 2>&1
 timeout 300 python scripts/fp32_modes.py > $O/fp32_modes.txt 2>&1
 ls -la $O
