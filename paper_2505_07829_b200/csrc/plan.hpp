@@ -97,6 +97,8 @@ KernelSpec f32x3_gemm_spec(int mode = 0, bool wide = false);  // 0 LayerNorm epi
 bool f32x3_wide(int64_t M, int64_t N);  // 128 x 256 output tiles for this launch
 bool f32x3_pair(int64_t M, int64_t N);  // 256 x 256 CTA-pair tiles for this launch
 KernelSpec f32x3_pair_spec(int mode);
+bool f32x3_pair_gate(int64_t M, int64_t F);  // K1 fp32 gate/up GEMM on CTA pairs (opt-in)
+KernelSpec f32x3_pair_gate_spec();
 KernelSpec simt_attn_spec();
 KernelSpec attn_f32_tiled_spec(int D, int Dv);
 bool attn_f32_tiled_supported(int64_t D, int64_t Dv);

@@ -187,7 +187,7 @@ static Plan make_plan_ffn(int64_t M, int64_t D, int64_t F, int64_t N, int dtype,
   std::ostringstream why;
   if (dtype == BF_DTYPE_F32) {
     const bool simt = env_int("BFGPU_F32_SIMT", 0) == 1;
-    p.spec = simt ? simt_gemm_spec(1) : f32x3_gemm_spec(1);
+    p.spec = simt ? simt_gemm_spec(1) : f32x3_pair_gate(M, (F + 31) / 32 * 32) ? f32x3_pair_gate_spec() : f32x3_gemm_spec(1);
     p.units = cdiv(M, p.spec.tile_m);
     p.tiles = p.units * (cdiv(F, p.spec.tile_n) + cdiv(N, p.spec.tile_n));
     p.resident_ctas = resident_ctas(p.spec);

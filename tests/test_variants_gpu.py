@@ -49,7 +49,7 @@ elif what == "f32pair":
     Vt = (rng.standard_normal((264, 136)) / 12).astype(np.float32).astype(np.float64)
     Ut = (rng.standard_normal((328, 264)) / 16).astype(np.float32).astype(np.float64)
     out = ops.rms_ffn_swiglu(f(X), f(Wt), f(Vt), f(Ut)).double().cpu().numpy()
-    assert_f32_close(out, cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 fp32 pair down GEMM")
+    assert_f32_close(out, cpu.rms_ffn_swiglu(X, Wt, Vt, Ut), "K1 fp32 pair gate/up and down GEMMs")
 elif what == "f32":
     # the FP32 FMA kernels (BFGPU_F32_SIMT=1) instead of the 3xTF32 tensor-core plans
     f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().float()
@@ -94,8 +94,8 @@ print("ok")
         ("attn", {"BFGPU_ATTN_EMU": "12"}),
         ("attn", {"BFGPU_ATTN_EMU": "16"}),
         ("f32", {"BFGPU_F32_SIMT": "1"}),
-        ("f32pair", {"BFGPU_F32_PAIR": "1"}),
-        ("f32pair", {"BFGPU_F32_PAIR": "1", "BFGPU_F32_GROUP": "1"}),
+        ("f32pair", {"BFGPU_F32_PAIR": "1", "BFGPU_F32_K1_PAIR": "1"}),
+        ("f32pair", {"BFGPU_F32_PAIR": "1", "BFGPU_F32_K1_PAIR": "1", "BFGPU_F32_GROUP": "1"}),
     ],
 )
 def test_variant_matches_oracle(what, env):
