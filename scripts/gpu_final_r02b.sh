@@ -1,8 +1,8 @@
 #!/bin/bash
 # Round-2 evidence (session 4, after the fp32-mode work): full GPU suite, smoke, every bench workload (with CPU baselines), the
 # reference arm, launch lists and ncu --set full captures of each product kernel.
-mkdir -p gpurun_out/final4
-O=gpurun_out/final4
+mkdir -p gpurun_out/final5
+O=gpurun_out/final5
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/nvsmi.txt
 timeout 1500 python -m pytest tests -m gpu -q -rf > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
