@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* vs_empty = vs_full + 1;
   uint64_t* q_ready = vs_empty + 1;
   uint64_t* s_full = q_ready + 1;
-  uint64_t* p_ready = s_full + 1;
-  uint64_t* o_full = p_ready + 1;
+  uint64_t* p_ready = s_full + 1;  // [2]: keys 0-31 and 32-63 of the block written to TMEM
+  uint64_t* o_full = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(vs_empty, 1);
     mbar_init(q_ready, 128);
     mbar_init(s_full, 1);
-    mbar_init(p_ready, 128);
+    mbar_init(&p_ready[0], 128);
+    mbar_init(&p_ready[1], 128);
     mbar_init(o_full, 1);
     fence_barrier_init();
   }
@@ -156,18 +157,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         umma_commit(s_full);
       }
       __syncwarp();
-      mbar_wait(p_ready, j & 1);
       mbar_wait(vs_full, j & 1);
-      tc_fence_after();
-      if (lane == 0) {
+      // PV in two halves of 32 keys: the first runs while the softmax writes the second
 #pragma unroll
-        for (int kk = 0; kk < BKV / 8; ++kk) {
-          const uint32_t bo = (kk >> 2) * (DV * 128) + (kk & 3) * 32;
-          const uint64_t bh = sdesc_kmajor_sw128(vs + bo), bl = sdesc_kmajor_sw128(vs + RAW_BYTES + bo);
-          umma_tf32_ts(tmem + COL_O, tmem + COL_PL + kk * 8, bh, IDESC_O, (j | kk) != 0);
-          umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bl, IDESC_O, 1);
-          umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bh, IDESC_O, 1);
+      for (int half = 0; half < 2; ++half) {
+        mbar_wait(&p_ready[half], j & 1);
+        tc_fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = 4 * half + k4;
+            const uint32_t bo = (kk >> 2) * (DV * 128) + (kk & 3) * 32;
+            const uint64_t bh = sdesc_kmajor_sw128(vs + bo), bl = sdesc_kmajor_sw128(vs + RAW_BYTES + bo);
+            umma_tf32_ts(tmem + COL_O, tmem + COL_PL + kk * 8, bh, IDESC_O, (j | kk) != 0);
+            umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bl, IDESC_O, 1);
+            umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bh, IDESC_O, 1);
+          }
         }
+        __syncwarp();
+      }
+      if (lane == 0) {
         umma_commit(vs_empty);
         if (j == nb - 1) umma_commit(o_full);
       }
@@ -278,11 +287,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tmem_st_32x32b_x32(tl + COL_S + 32 * half, ph);
         tmem_st_32x32b_x32(tl + COL_PL + 32 * half, pl);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_ready[half]);  // (half 0 also covers the O rebase above)
       }
       l_run += ls;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_ready);
     }
     mbar_wait(o_full, 0);
     tc_fence_after();
