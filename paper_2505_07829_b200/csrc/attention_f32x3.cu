@@ -11,14 +11,16 @@
 // safe_attention_rows, safe_numerics.hpp:158-170).
 //
 // The bf_attention C-ABI has no workspace, so the operands are split inside the kernel: TMA
-// brings raw fp32 key and value blocks into a 3-slot ring, and four converter warps write hi
+// brings raw fp32 key and value blocks into a 2-slot ring, and four converter warps write hi
 // and lo at the same swizzled offsets (the split is elementwise, so the SW128 layout carries
-// over) into single-buffered split tiles, one block ahead of the MMAs.
+// over) into single-buffered split tiles, one block ahead of the MMAs. S is double-buffered in
+// TMEM, so S(j+1) runs on the tensor pipe while the softmax works on S(j); P_hi overwrites its
+// S buffer and P_lo goes to SMEM (an SS operand of PV).
 //
 // One CTA per (head, 128 query rows); 384 threads:
 //   warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
 //   warps 4-7 softmax + epilogue (thread = query row = TMEM lane), warps 8-11 converters.
-// TMEM (512 columns): Q_hi [0, D) | Q_lo [D, 2D) | S, then P_hi [2D, 2D+64) | P_lo [+64, +128) | O [2D+128, +Dv).
+// TMEM (512 columns): Q_hi [0, D) | Q_lo [D, 2D) | S/P_hi x2 [2D, 2D+128) | O [2D+128, +Dv).
 // Block program: the final snapshot of fuse(lower(examples::attention())) (lowering.hpp:559-571).
 #include <cuda_runtime.h>
 
@@ -34,12 +36,14 @@ namespace attn_f32x3 {
 
 constexpr int BQ = 128, BKV = 64;
 constexpr int THREADS = 384;
-constexpr int RAW_SLOTS = 3;
+constexpr int RAW_SLOTS = 2;
 constexpr int RAW_BYTES = 32768;  // one raw block: 64 keys x D (<= 128) fp32, or Dv (<= 128) x 64 keys
 constexpr int SPLIT_BYTES = 2 * RAW_BYTES;  // hi | lo
 constexpr int OFF_KS = RAW_SLOTS * RAW_BYTES;
 constexpr int OFF_VS = OFF_KS + SPLIT_BYTES;
-constexpr int OFF_BAR = OFF_VS + SPLIT_BYTES;
+constexpr int OFF_PL = OFF_VS + SPLIT_BYTES;  // P_lo [128 rows][64 keys], two SW128 boxes of 32 keys
+constexpr int PL_BYTES = 128 * 64 * 4;
+constexpr int OFF_BAR = OFF_PL + PL_BYTES;
 constexpr int SMEM = OFF_BAR + 256;
 static_assert(SMEM <= 232448, "fp32 tensor-core attention SMEM budget");
 
@@ -58,10 +62,39 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 
+// D[tmem] (+)= A[smem] * B[smem]^T, tf32.
+__device__ __forceinline__ void umma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// Order of the raw ring: K0, K1, V0, K2, V1, ..., K(nb-1), V(nb-2), V(nb-1). Each key block is
+// split one step ahead of the value block before it, so S(j+1) can be issued while PV(j-1) runs.
+__device__ __forceinline__ void ring_item(int n, int nb, bool& is_k, int& j) {
+  if (n == 0) {
+    is_k = true;
+    j = 0;
+    return;
+  }
+  const int m = n - 1;
+  if (m / 2 + 1 < nb) {
+    is_k = (m & 1) == 0;
+    j = is_k ? m / 2 + 1 : m / 2;
+  } else {
+    is_k = false;
+    j = n - nb;
+  }
 }
 
 template <int D, int DV>
@@ -71,7 +104,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   using namespace dev;
   static_assert((D == 64 || D == 128) && (DV == 64 || DV == 128), "head dims 64/128");
   constexpr int K_BYTES = BKV * D * 4, V_BYTES = DV * BKV * 4;
-  constexpr uint32_t COL_QH = 0, COL_QL = D, COL_S = 2 * D, COL_PL = 2 * D + 64, COL_O = 2 * D + 128;
+  // S is double-buffered (S(j+1) runs while the softmax works on S(j)); P_hi overwrites its S
+  // buffer, P_lo goes to SMEM
+  constexpr uint32_t COL_QH = 0, COL_QL = D, COL_S = 2 * D, COL_O = 2 * D + 128;
   static_assert(COL_O + DV <= 512, "TMEM budget");
   constexpr uint32_t IDESC_S = idesc_tf32(BQ, BKV), IDESC_O = idesc_tf32(BQ, DV);
 
@@ -84,9 +119,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* vs_full = ks_empty + 1;
   uint64_t* vs_empty = vs_full + 1;
   uint64_t* q_ready = vs_empty + 1;
-  uint64_t* s_full = q_ready + 1;
-  uint64_t* p_ready = s_full + 1;  // [2]: keys 0-31 and 32-63 of the block written to TMEM
-  uint64_t* o_full = p_ready + 2;
+  uint64_t* s_full = q_ready + 1;   // [2]: one per S buffer
+  uint64_t* p_ready = s_full + 2;  // [2]: keys 0-31 and 32-63 of the block written
+  uint64_t* pv_done = p_ready + 2;
+  uint64_t* o_full = pv_done + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
@@ -106,7 +142,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(vs_full, 128);
     mbar_init(vs_empty, 1);
     mbar_init(q_ready, 128);
-    mbar_init(s_full, 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(pv_done, 1);
     mbar_init(&p_ready[0], 128);
     mbar_init(&p_ready[1], 128);
     mbar_init(o_full, 1);
@@ -119,13 +157,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---- TMA: K(j) then V(j) into the raw ring
+    // ---- TMA: key and value blocks into the raw ring, in ring_item order
     if (lane == 0) {
       for (int i = 0; i < 2 * nb; ++i) {
-        const int s = i % RAW_SLOTS, j = i >> 1;
+        const int s = i % RAW_SLOTS;
+        bool is_k;
+        int j;
+        ring_item(i, nb, is_k, j);
         mbar_wait(&empty[s], ((i / RAW_SLOTS) & 1) ^ 1);
         uint8_t* dst = smem + s * RAW_BYTES;
-        if ((i & 1) == 0) {
+        if (is_k) {
           mbar_arrive_expect_tx(&full[s], K_BYTES);
 #pragma unroll
           for (int b = 0; b < D / 32; ++b) tma_load_3d(&tm_k, &full[s], dst + b * (BKV * 128), 32 * b, j * BKV, h);
@@ -138,25 +179,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // ---- MMA issuer
-    const uint32_t ks = smem_u32(smem + OFF_KS), vs = smem_u32(smem + OFF_VS);
-    mbar_wait(q_ready, 0);
-    for (int j = 0; j < nb; ++j) {
+    const uint32_t ks = smem_u32(smem + OFF_KS), vs = smem_u32(smem + OFF_VS), pls = smem_u32(smem + OFF_PL);
+    auto issue_s = [&](int j) {  // S(j) into buffer j & 1
       mbar_wait(ks_full, j & 1);
       tc_fence_after();
       if (lane == 0) {
+        const uint32_t sb = tmem + COL_S + (j & 1) * 64;
 #pragma unroll
         for (int kk = 0; kk < D / 8; ++kk) {
           const uint32_t bo = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
           const uint64_t bh = sdesc_kmajor_sw128(ks + bo), bl = sdesc_kmajor_sw128(ks + RAW_BYTES + bo);
           // small terms first: lo*hi, hi*lo, then hi*hi
-          umma_tf32_ts(tmem + COL_S, tmem + COL_QL + kk * 8, bh, IDESC_S, kk != 0);
-          umma_tf32_ts(tmem + COL_S, tmem + COL_QH + kk * 8, bl, IDESC_S, 1);
-          umma_tf32_ts(tmem + COL_S, tmem + COL_QH + kk * 8, bh, IDESC_S, 1);
+          umma_tf32_ts(sb, tmem + COL_QL + kk * 8, bh, IDESC_S, kk != 0);
+          umma_tf32_ts(sb, tmem + COL_QH + kk * 8, bl, IDESC_S, 1);
+          umma_tf32_ts(sb, tmem + COL_QH + kk * 8, bh, IDESC_S, 1);
         }
         umma_commit(ks_empty);
-        umma_commit(s_full);
+        umma_commit(&s_full[j & 1]);
       }
       __syncwarp();
+    };
+    mbar_wait(q_ready, 0);
+    issue_s(0);
+    for (int j = 0; j < nb; ++j) {
+      if (j + 1 < nb) issue_s(j + 1);  // runs on the tensor pipe while the softmax works on S(j)
       mbar_wait(vs_full, j & 1);
       // PV in two halves of 32 keys: the first runs while the softmax writes the second
 #pragma unroll
@@ -164,20 +210,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&p_ready[half], j & 1);
         tc_fence_after();
         if (lane == 0) {
+          const uint32_t pb = tmem + COL_S + (j & 1) * 64;  // P_hi over S(j)
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = 4 * half + k4;
             const uint32_t bo = (kk >> 2) * (DV * 128) + (kk & 3) * 32;
             const uint64_t bh = sdesc_kmajor_sw128(vs + bo), bl = sdesc_kmajor_sw128(vs + RAW_BYTES + bo);
-            umma_tf32_ts(tmem + COL_O, tmem + COL_PL + kk * 8, bh, IDESC_O, (j | kk) != 0);
-            umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bl, IDESC_O, 1);
-            umma_tf32_ts(tmem + COL_O, tmem + COL_S + kk * 8, bh, IDESC_O, 1);
+            const uint64_t pl = sdesc_kmajor_sw128(pls + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+            umma_tf32_ss(tmem + COL_O, pl, bh, IDESC_O, (j | kk) != 0);
+            umma_tf32_ts(tmem + COL_O, pb + kk * 8, bl, IDESC_O, 1);
+            umma_tf32_ts(tmem + COL_O, pb + kk * 8, bh, IDESC_O, 1);
           }
         }
         __syncwarp();
       }
       if (lane == 0) {
         umma_commit(vs_empty);
+        umma_commit(pv_done);
         if (j == nb - 1) umma_commit(o_full);
       }
       __syncwarp();
@@ -186,8 +235,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- converters: raw block -> hi | lo at the same swizzled offsets
     const int t = static_cast<int>(threadIdx.x) - 256;
     for (int i = 0; i < 2 * nb; ++i) {
-      const int s = i % RAW_SLOTS, j = i >> 1;
-      const bool is_k = (i & 1) == 0;
+      const int s = i % RAW_SLOTS;
+      bool is_k;
+      int j;
+      ring_item(i, nb, is_k, j);
       mbar_wait(&full[s], (i / RAW_SLOTS) & 1);
       mbar_wait(is_k ? ks_empty : vs_empty, (j & 1) ^ 1);
       const float4* src = reinterpret_cast<const float4*>(smem + s * RAW_BYTES);
@@ -235,11 +286,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nb; ++j) {
-      mbar_wait(s_full, j & 1);  // also: PV(j-1) complete (same issuer, committed after it)
+      const uint32_t sb = COL_S + (j & 1) * 64;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       uint32_t s0[32], s1[32];
-      tmem_ld_32x32b_x32(tl + COL_S, s0);
-      tmem_ld_32x32b_x32(tl + COL_S + 32, s1);
+      tmem_ld_32x32b_x32(tl + sb, s0);
+      tmem_ld_32x32b_x32(tl + sb + 32, s1);
       tmem_wait_ld();
       const int valid = Skv - j * BKV;  // keys of this block that exist
       float x[64];
@@ -259,6 +311,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // takes the branch and rows that keep their base scale by 1.
         const bool grow = mx > m_run + 8.0f;
         if (__any_sync(0xffffffffu, grow)) {
+          mbar_wait(pv_done, (j - 1) & 1);  // O holds PV(0..j-1) only once PV(j-1) is complete
+          tc_fence_after();
           const float f = grow ? ex2_approx(m_run - mx) : 1.0f;
           l_run *= f;
 #pragma unroll 1
@@ -274,19 +328,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       float ls = 0.f;
-      uint32_t ph[32], pl[32];
+      uint8_t* plrow = smem + OFF_PL + row * 128;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
+        uint32_t ph[32];
+        float pl[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const float p = ex2_approx(x[32 * half + c] - m_run);
           ls += p;
           const float hh = tf32_hi(p);
           ph[c] = __float_as_uint(hh);
-          pl[c] = __float_as_uint(p - hh);
+          pl[c] = p - hh;
         }
-        tmem_st_32x32b_x32(tl + COL_S + 32 * half, ph);
-        tmem_st_32x32b_x32(tl + COL_PL + 32 * half, pl);
+        tmem_st_32x32b_x32(tl + sb + 32 * half, ph);
+        // P_lo of PV(j-1) must be consumed before it is overwritten
+        if (half == 0 && j > 0) mbar_wait(pv_done, (j - 1) & 1);
+        uint8_t* box = plrow + half * (128 * 128);  // keys 32 half .. +31: one SW128 box
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(box + ((c ^ (row & 7)) << 4)) =
+              make_float4(pl[4 * c], pl[4 * c + 1], pl[4 * c + 2], pl[4 * c + 3]);
+        fence_proxy_async_smem();
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_ready[half]);  // (half 0 also covers the O rebase above)
